@@ -1,0 +1,584 @@
+// C ABI of libvecchia_b200.so (include/vecchia_b200.h): argument checking,
+// device memory of a plan, host<->device staging and status mapping.  All
+// arithmetic happens in the sm_100a kernels of the sibling .cu files; there is
+// no host compute path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vgp_internal.cuh"
+
+namespace vgp {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// Taylor coefficients of 1/Gamma(1+x) about 0 (a_0 .. a_24), mpmath at 50 digits.
+static const double kRecipGammaTaylor[25] = {
+    0x1.0000000000000p+0,   0x1.2788cfc6fb619p-1,  -0x1.4fcf4026afa2ep-1, -0x1.5815e8fa27048p-5,
+    0x1.5512320b43fbep-3,  -0x1.59af103c34092p-5,  -0x1.3b4af28483e21p-7, 0x1.d919c527f60b2p-8,
+    -0x1.317112ce3a2a8p-10, -0x1.c364fe6f1563dp-13, 0x1.0c8a78cd9f9d2p-13, -0x1.51ce8af47eabep-16,
+    -0x1.4fad41fc34fbbp-20, 0x1.302509dbc0de3p-20, -0x1.b9986666c225dp-23, 0x1.a44b7ba22d629p-28,
+    0x1.57bc3fc384334p-28,  -0x1.44b4cedca388fp-30, 0x1.cae7675c18607p-34, 0x1.11d065bfaf067p-37,
+    -0x1.0423bac8ca3fbp-38, 0x1.1f20151323cd0p-41, -0x1.72cb88ea5ae6ep-46, -0x1.815f72a05f16fp-48,
+    0x1.6198491a83bcdp-50};
+
+void fill_bessel(double nu, CovParams* c);
+
+int make_cov_params(int family, double s2, double beta, double nu, CovParams* c) {
+  // KernelParams validation, vg/kernels.py:31-35
+  if (!(std::isfinite(s2) && s2 > 0.0) || !(std::isfinite(beta) && beta > 0.0) ||
+      !(std::isfinite(nu) && nu > 0.0))
+    return fail(VGP_E_INVALID, "sigma_sq, beta and nu must be finite and > 0");
+  std::memset(c, 0, sizeof(*c));
+  c->s2 = s2;
+  c->beta = beta;
+  c->inv_beta = 1.0 / beta;
+  c->nu = nu;
+  if (family == VGP_FAMILY_POWEXP) {
+    c->kind = kPowExp;
+    return VGP_OK;
+  }
+  if (family != VGP_FAMILY_MATERN) return fail(VGP_E_INVALID, "unknown kernel family");
+  // closed forms by exact equality, vg/kernels.py:69-74
+  if (nu == 0.5) {
+    c->kind = kMatern05;
+  } else if (nu == 1.5) {
+    c->kind = kMatern15;
+  } else if (nu == 2.5) {
+    c->kind = kMatern25;
+  } else {
+    c->kind = kMaternGen;
+    c->coef = std::pow(2.0, 1.0 - nu) / std::tgamma(nu);  // 2^(1-nu)/Gamma(nu), vg/kernels.py:81
+    fill_bessel(nu, c);
+  }
+  return VGP_OK;
+}
+
+int make_bessel_params(double nu, CovParams* c) {
+  if (!(std::isfinite(nu) && nu >= 0.0)) return fail(VGP_E_INVALID, "nu must be finite and >= 0");
+  std::memset(c, 0, sizeof(*c));
+  c->kind = kMaternGen;
+  c->nu = nu;
+  fill_bessel(nu, c);
+  return VGP_OK;
+}
+
+void fill_bessel(double nu, CovParams* c) {
+  {
+    int nl = (int)(nu + 0.5);
+    double mu = nu - nl;
+    c->nl = nl;
+    c->mu = mu;
+    // f(x) = 1/Gamma(1+x); gampl = f(mu), gammi = f(-mu),
+    // gam1 = (f(-mu) - f(mu)) / (2 mu) = -sum_{k odd} a_k mu^(k-1),
+    // gam2 = (f(-mu) + f(mu)) / 2     =  sum_{k even} a_k mu^k
+    double fp = 0.0, fm = 0.0, g1 = 0.0, g2 = 0.0;
+    for (int k = 24; k >= 0; --k) {
+      fp = fp * mu + kRecipGammaTaylor[k];
+      fm = fm * (-mu) + kRecipGammaTaylor[k];
+    }
+    for (int k = 23; k >= 1; k -= 2) g1 = g1 * (mu * mu) + kRecipGammaTaylor[k];
+    for (int k = 24; k >= 0; k -= 2) g2 = g2 * (mu * mu) + kRecipGammaTaylor[k];
+    c->gampl = fp;
+    c->gammi = fm;
+    c->gam1 = -g1;
+    c->gam2 = g2;
+    double pimu = kPi * mu;
+    c->fact = std::fabs(pimu) < 1e-16 ? 1.0 : pimu / std::sin(pimu);
+  }
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int check_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(VGP_E_CUDA, std::string("no CUDA device available (") +
+                                (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                                "); the B200 path has no CPU fallback");
+  if (device < 0 || device >= count) return fail(VGP_E_INVALID, "device ordinal out of range");
+  return VGP_OK;
+}
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * count);
+  if (e != cudaSuccess) return fail(VGP_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return VGP_OK;
+}
+
+void free_plan(Plan* p) {
+  if (!p) return;
+  cudaFree(p->d_order);
+  cudaFree(p->d_nbr);
+  cudaFree(p->d_pts);
+  cudaFree(p->d_raw);
+  cudaFree(p->d_rest);
+  cudaFree(p->d_mu);
+  cudaFree(p->d_sig);
+  cudaFree(p->d_partials);
+  cudaFree(p->d_scalars);
+  cudaFree(p->d_fail);
+  cudaFree(p->d_work);
+  if (p->h_stage) cudaFreeHost(p->h_stage);
+  if (p->h_small) cudaFreeHost(p->h_small);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+// Launch the full evaluation sequence on the plan's stream.
+int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
+  cudaStream_t s = p->stream;
+  VGP_CUDA_TRY(cudaMemsetAsync(p->d_fail, 0xff, 2 * sizeof(unsigned long long), s));
+  int64_t e_lo = p->blk_lo, e_hi = p->blk_hi;
+  if (e_lo == 0) {
+    VGP_CUDA_TRY(launch_loglik_generic(*p, cp, 0, 1, s));
+    e_lo = 1;
+  } else {
+    VGP_CUDA_TRY(cudaMemsetAsync(p->d_scalars + 1, 0, sizeof(double), s));
+  }
+  if (e_hi > e_lo) {
+    bool use_dmma = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
+    if (p->force_variant == 0) use_dmma = false;
+    if (p->force_variant == 1 && !use_dmma)
+      return fail(VGP_E_UNSUPPORTED, "warp-DMMA variant does not cover this m / kernel");
+    if (use_dmma) {
+      VGP_CUDA_TRY(launch_loglik_dmma(*p, cp, e_lo, e_hi, s));
+      p->kernel_variant = 1;
+    } else {
+      VGP_CUDA_TRY(launch_loglik_generic(*p, cp, e_lo, e_hi, s));
+      p->kernel_variant = 0;
+    }
+  }
+  VGP_CUDA_TRY(launch_reduce(*p, want_total, s));
+  return VGP_OK;
+}
+
+int decode_status(const Plan* p, const unsigned long long* flags, int64_t* fail_index) {
+  if (flags[0] != ~0ull) {
+    if (fail_index) *fail_index = npd_key_entry(flags[0], p->m);
+    return VGP_NOT_POSITIVE_DEFINITE;
+  }
+  if (flags[1] != ~0ull) {
+    if (fail_index) *fail_index = (int64_t)flags[1];
+    return VGP_BAD_CONDITIONAL_VARIANCE;
+  }
+  if (fail_index) *fail_index = -1;
+  return VGP_OK;
+}
+
+}  // namespace
+}  // namespace vgp
+
+using namespace vgp;
+
+struct vgp_plan {
+  Plan p;
+};
+
+extern "C" {
+
+const char* vgp_version(void) { return "vecchia_b200 0.1.0 (sm_100a)"; }
+
+const char* vgp_last_error(void) { return g_last_error.c_str(); }
+
+int vgp_device_count(int* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) c = 0;
+  if (count) *count = c;
+  return VGP_OK;
+}
+
+int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t m,
+                         int64_t* neighbors) {
+  if (!locations || !neighbors) return fail(VGP_E_INVALID, "null pointer");
+  if (m < 1 || n <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
+  if (n > (int64_t)INT32_MAX) return fail(VGP_E_INVALID, "n exceeds int32 index range");
+  int rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  cudaStream_t s;
+  VGP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double2* d_pts = nullptr;
+  int64_t* d_out = nullptr;
+  double* d_keys = nullptr;
+  int32_t* d_idx = nullptr;
+  const int64_t nq = n - m;
+  const int64_t batch = std::min<int64_t>(nq, int64_t(1) << 20);
+  const int64_t slots = ((batch + 127) / 128) * 128;
+  rc = dalloc(&d_pts, n);
+  if (!rc) rc = dalloc(&d_out, (size_t)batch * m);
+  if (!rc) rc = dalloc(&d_keys, (size_t)slots * m);
+  if (!rc) rc = dalloc(&d_idx, (size_t)slots * m);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
+  for (int64_t q0 = 0; !rc && e == cudaSuccess && q0 < nq; q0 += batch) {
+    int64_t qn = std::min(batch, nq - q0);
+    e = launch_knn(d_pts, n, d_pts + m + q0, qn, q0, 1, m, d_out, d_keys, d_idx, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(neighbors + q0 * m, d_out, sizeof(int64_t) * qn * m,
+                          cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn: ") + cudaGetErrorString(e));
+  cudaFree(d_pts);
+  cudaFree(d_out);
+  cudaFree(d_keys);
+  cudaFree(d_idx);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+int vgp_knn_points(int device, const double* query, int64_t nq, const double* data, int64_t nd,
+                   int32_t m, int64_t* neighbors) {
+  if (!query || !data || !neighbors) return fail(VGP_E_INVALID, "null pointer");
+  if (m < 1 || m > nd) return fail(VGP_E_INVALID, "need 1 <= m <= nd");
+  if (nq <= 0) return VGP_OK;
+  int rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  cudaStream_t s;
+  VGP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double2 *d_data = nullptr, *d_q = nullptr;
+  int64_t* d_out = nullptr;
+  double* d_keys = nullptr;
+  int32_t* d_idx = nullptr;
+  const int64_t batch = std::min<int64_t>(nq, int64_t(1) << 20);
+  const int64_t slots = ((batch + 127) / 128) * 128;
+  rc = dalloc(&d_data, nd);
+  if (!rc) rc = dalloc(&d_q, nq);
+  if (!rc) rc = dalloc(&d_out, (size_t)batch * m);
+  if (!rc) rc = dalloc(&d_keys, (size_t)slots * m);
+  if (!rc) rc = dalloc(&d_idx, (size_t)slots * m);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpyAsync(d_data, data, sizeof(double2) * nd, cudaMemcpyHostToDevice, s);
+  if (!rc && e == cudaSuccess)
+    e = cudaMemcpyAsync(d_q, query, sizeof(double2) * nq, cudaMemcpyHostToDevice, s);
+  for (int64_t q0 = 0; !rc && e == cudaSuccess && q0 < nq; q0 += batch) {
+    int64_t qn = std::min(batch, nq - q0);
+    e = launch_knn(d_data, nd, d_q + q0, qn, q0, 0, m, d_out, d_keys, d_idx, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(neighbors + q0 * m, d_out, sizeof(int64_t) * qn * m,
+                          cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn: ") + cudaGetErrorString(e));
+  cudaFree(d_data);
+  cudaFree(d_q);
+  cudaFree(d_out);
+  cudaFree(d_keys);
+  cudaFree(d_idx);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+int vgp_cov(int device, int family, double sigma_sq, double beta, double nu, const double* d,
+            int64_t count, double* out) {
+  if (count < 0 || (count > 0 && (!d || !out))) return fail(VGP_E_INVALID, "bad arguments");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  if (count == 0) return VGP_OK;
+  rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  double *d_in = nullptr, *d_out = nullptr;
+  rc = dalloc(&d_in, count);
+  if (!rc) rc = dalloc(&d_out, count);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpy(d_in, d, sizeof(double) * count, cudaMemcpyHostToDevice);
+  if (!rc && e == cudaSuccess) e = launch_cov_eval(cp, d_in, count, d_out, 0);
+  if (!rc && e == cudaSuccess) e = cudaMemcpy(out, d_out, sizeof(double) * count, cudaMemcpyDeviceToHost);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("cov: ") + cudaGetErrorString(e));
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return rc;
+}
+
+int vgp_bessel_kv(int device, double nu, const double* x, int64_t count, double* out) {
+  if (count < 0 || (count > 0 && (!x || !out))) return fail(VGP_E_INVALID, "bad arguments");
+  CovParams cp;
+  int rc = make_bessel_params(nu, &cp);
+  if (rc) return rc;
+  for (int64_t i = 0; i < count; ++i)
+    if (!(x[i] > 0.0)) return fail(VGP_E_INVALID, "bessel_kv requires x > 0");
+  if (count == 0) return VGP_OK;
+  rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  double *d_in = nullptr, *d_out = nullptr;
+  rc = dalloc(&d_in, count);
+  if (!rc) rc = dalloc(&d_out, count);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpy(d_in, x, sizeof(double) * count, cudaMemcpyHostToDevice);
+  if (!rc && e == cudaSuccess) e = launch_bessel_eval(cp, d_in, count, d_out, 0);
+  if (!rc && e == cudaSuccess) e = cudaMemcpy(out, d_out, sizeof(double) * count, cudaMemcpyDeviceToHost);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("bessel_kv: ") + cudaGetErrorString(e));
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return rc;
+}
+
+int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
+                    const int64_t* order, const int64_t* neighbors, int64_t block_lo,
+                    int64_t block_hi, vgp_plan** out) {
+  if (!out || !order) return fail(VGP_E_INVALID, "null pointer");
+  *out = nullptr;
+  if (m < 1 || n <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
+  if (n > (int64_t)INT32_MAX) return fail(VGP_E_INVALID, "n exceeds int32 index range");
+  const int64_t count = n - m + 1;
+  if (block_lo < 0 || block_hi > count || block_lo >= block_hi)
+    return fail(VGP_E_INVALID, "block range outside [0, n - m + 1)");
+  if (metric != VGP_METRIC_EUCLIDEAN && metric != VGP_METRIC_GREAT_CIRCLE)
+    return fail(VGP_E_INVALID, "unknown metric");
+  const int64_t rest_lo = std::max<int64_t>(block_lo, 1) - 1;
+  const int64_t rest_hi = block_hi - 1;
+  if (rest_hi > rest_lo && !neighbors) return fail(VGP_E_INVALID, "null neighbour table");
+  if (rest_lo % kReduceChunk != 0)
+    return fail(VGP_E_INVALID, "shard must start on a 4096-entry reduction chunk boundary");
+  if (rest_hi < count - 1 && rest_hi % kReduceChunk != 0)
+    return fail(VGP_E_INVALID, "shard must end on a 4096-entry reduction chunk boundary");
+  int rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  Plan* p = new Plan();
+  p->device = device;
+  p->n = n;
+  p->m = m;
+  p->metric = metric;
+  p->radius = radius;
+  p->blk_lo = block_lo;
+  p->blk_hi = block_hi;
+  p->rest_lo = rest_lo;
+  p->rest_hi = std::max(rest_hi, rest_lo);
+  p->chunk_lo = rest_lo / kReduceChunk;
+  p->chunk_hi = (p->rest_hi + kReduceChunk - 1) / kReduceChunk;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t nrest = p->rest_hi - p->rest_lo;
+  cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return fail(VGP_E_CUDA, cudaGetErrorString(e));
+  }
+  rc = dalloc(&p->d_order, n);
+  if (!rc) rc = dalloc(&p->d_nbr, (size_t)nrest * m);
+  if (!rc) rc = dalloc(&p->d_pts, n);
+  if (!rc) rc = dalloc(&p->d_raw, (size_t)n * 3);
+  if (!rc) rc = dalloc(&p->d_rest, nrest);
+  if (!rc) rc = dalloc(&p->d_mu, nrest);
+  if (!rc) rc = dalloc(&p->d_sig, nrest);
+  if (!rc) rc = dalloc(&p->d_partials, std::max<int64_t>(p->chunk_hi - p->chunk_lo, 1));
+  if (!rc) rc = dalloc(&p->d_scalars, 4);
+  if (!rc) rc = dalloc(&p->d_fail, 2);
+  if (!rc) {
+    // generic-path global workspace when a block does not fit in shared memory
+    const int P = m + 2;
+    size_t mat = (size_t)(P | 1) * P;
+    if (sizeof(double) * (mat + 3 * (m + 1)) > 200 * 1024) {
+      int slots = p->num_sms * 2;
+      int64_t need = std::max<int64_t>(nrest, 1);
+      if (need < slots) slots = (int)need;
+      p->work_slots = slots;
+      p->work_doubles = mat * slots;
+      rc = dalloc(&p->d_work, p->work_doubles);
+    }
+  }
+  if (!rc && cudaMallocHost((void**)&p->h_small, 64) != cudaSuccess)
+    rc = fail(VGP_E_NOMEM, "cudaMallocHost small");
+  if (rc) {
+    free_plan(p);
+    return rc;
+  }
+  e = cudaMemcpyAsync(p->d_order, order, sizeof(int64_t) * n, cudaMemcpyHostToDevice, p->stream);
+  if (e == cudaSuccess && nrest > 0) {
+    // int64 -> int32 neighbour rows of this shard, via the pinned stage
+    std::vector<int32_t> tmp((size_t)nrest * m);
+    const int64_t* src = neighbors + rest_lo * (int64_t)m;
+    for (size_t i = 0; i < tmp.size(); ++i) {
+      int64_t v = src[i];
+      if (v < 0 || v >= n) {
+        free_plan(p);
+        return fail(VGP_E_INVALID, "neighbour index out of range");
+      }
+      tmp[i] = (int32_t)v;
+    }
+    e = cudaMemcpyAsync(p->d_nbr, tmp.data(), sizeof(int32_t) * tmp.size(), cudaMemcpyHostToDevice,
+                        p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return fail(VGP_E_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  }
+  vgp_plan* h = new vgp_plan();
+  h->p = *p;
+  delete p;  // ownership of the device buffers moved into h->p
+  *out = h;
+  return VGP_OK;
+}
+
+int vgp_plan_set_data(vgp_plan* plan, const double* locations, const double* observations) {
+  if (!plan || !locations || !observations) return fail(VGP_E_INVALID, "null pointer");
+  Plan* p = &plan->p;
+  DeviceGuard g(p->device);
+  const int64_t n = p->n;
+  // (x, y) rows then observations, straight from the caller's arrays
+  VGP_CUDA_TRY(cudaMemcpyAsync(p->d_raw, locations, sizeof(double) * 2 * n, cudaMemcpyHostToDevice,
+                               p->stream));
+  VGP_CUDA_TRY(cudaMemcpyAsync(p->d_raw + 2 * n, observations, sizeof(double) * n,
+                               cudaMemcpyHostToDevice, p->stream));
+  VGP_CUDA_TRY(launch_permute(p->d_raw, p->d_order, n, p->d_pts, p->stream));
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  p->has_data = true;
+  return VGP_OK;
+}
+
+int vgp_plan_destroy(vgp_plan* plan) {
+  if (!plan) return VGP_OK;
+  DeviceGuard g(plan->p.device);
+  Plan* p = new Plan(plan->p);
+  free_plan(p);
+  delete plan;
+  return VGP_OK;
+}
+
+int vgp_plan_info(const vgp_plan* plan, int64_t* info) {
+  if (!plan || !info) return fail(VGP_E_INVALID, "null pointer");
+  const Plan& p = plan->p;
+  info[0] = p.n;
+  info[1] = p.m;
+  info[2] = p.blk_lo;
+  info[3] = p.blk_hi;
+  info[4] = p.chunk_lo;
+  info[5] = p.chunk_hi - p.chunk_lo;
+  info[6] = p.kernel_variant;
+  info[7] = p.device;
+  return VGP_OK;
+}
+
+int vgp_plan_set_variant(vgp_plan* plan, int variant) {
+  if (!plan || variant < -1 || variant > 1) return fail(VGP_E_INVALID, "bad variant");
+  plan->p.force_variant = variant;
+  return VGP_OK;
+}
+
+void* vgp_plan_stream(vgp_plan* plan) { return plan ? (void*)plan->p.stream : nullptr; }
+
+int vgp_loglik_async(vgp_plan* plan, int family, double sigma_sq, double beta, double nu) {
+  if (!plan) return fail(VGP_E_INVALID, "null plan");
+  Plan* p = &plan->p;
+  if (!p->has_data) return fail(VGP_E_INVALID, "plan has no data (vgp_plan_set_data)");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  DeviceGuard g(p->device);
+  const bool full = p->blk_lo == 0 && p->blk_hi == p->n - p->m + 1;
+  return launch_eval(p, cp, full);
+}
+
+int vgp_plan_fetch(vgp_plan* plan, double* total, int64_t* fail_index, int* status) {
+  if (!plan) return fail(VGP_E_INVALID, "null plan");
+  Plan* p = &plan->p;
+  DeviceGuard g(p->device);
+  unsigned long long* flags = (unsigned long long*)p->h_small;
+  double* sc = p->h_small + 2;
+  VGP_CUDA_TRY(cudaMemcpyAsync(flags, p->d_fail, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaMemcpyAsync(sc, p->d_scalars, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  int st = decode_status(p, flags, fail_index);
+  if (status) *status = st;
+  if (total) *total = st == VGP_OK ? sc[0] : NAN;
+  return VGP_OK;
+}
+
+int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
+               double* total, int64_t* fail_index, double* block_first, double* block_rest,
+               double* mu_new, double* sigma_new) {
+  if (!plan) return fail(VGP_E_INVALID, "null plan");
+  Plan* p = &plan->p;
+  if (!(p->blk_lo == 0 && p->blk_hi == p->n - p->m + 1))
+    return fail(VGP_E_INVALID, "vgp_loglik needs a plan over all blocks; use vgp_loglik_partials");
+  if (!p->has_data) return fail(VGP_E_INVALID, "plan has no data (vgp_plan_set_data)");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  DeviceGuard g(p->device);
+  rc = launch_eval(p, cp, true);
+  if (rc) return rc;
+  const int64_t nrest = p->rest_hi - p->rest_lo;
+  unsigned long long* flags = (unsigned long long*)p->h_small;
+  double* sc = p->h_small + 2;
+  VGP_CUDA_TRY(cudaMemcpyAsync(flags, p->d_fail, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaMemcpyAsync(sc, p->d_scalars, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  if (block_rest)
+    VGP_CUDA_TRY(cudaMemcpyAsync(block_rest, p->d_rest, sizeof(double) * nrest,
+                                 cudaMemcpyDeviceToHost, p->stream));
+  if (mu_new)
+    VGP_CUDA_TRY(cudaMemcpyAsync(mu_new, p->d_mu, sizeof(double) * nrest, cudaMemcpyDeviceToHost,
+                                 p->stream));
+  if (sigma_new)
+    VGP_CUDA_TRY(cudaMemcpyAsync(sigma_new, p->d_sig, sizeof(double) * nrest,
+                                 cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  int st = decode_status(p, flags, fail_index);
+  if (total) *total = st == VGP_OK ? sc[0] : NAN;
+  if (block_first) *block_first = st == VGP_OK ? sc[1] : NAN;
+  return st;
+}
+
+int vgp_loglik_partials(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
+                        double* partials, double* block_first, int64_t* fail_index) {
+  if (!plan) return fail(VGP_E_INVALID, "null plan");
+  Plan* p = &plan->p;
+  if (!p->has_data) return fail(VGP_E_INVALID, "plan has no data (vgp_plan_set_data)");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  DeviceGuard g(p->device);
+  rc = launch_eval(p, cp, false);
+  if (rc) return rc;
+  unsigned long long* flags = (unsigned long long*)p->h_small;
+  double* sc = p->h_small + 2;
+  VGP_CUDA_TRY(cudaMemcpyAsync(flags, p->d_fail, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaMemcpyAsync(sc, p->d_scalars, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  if (partials)
+    VGP_CUDA_TRY(cudaMemcpyAsync(partials, p->d_partials,
+                                 sizeof(double) * (p->chunk_hi - p->chunk_lo),
+                                 cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  int st = decode_status(p, flags, fail_index);
+  if (block_first) *block_first = p->blk_lo == 0 ? sc[1] : 0.0;
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+// Internal declarations shared by the sm_100a translation units of
+// libvecchia_b200.so.  Nothing here crosses the C ABI (include/vecchia_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "vecchia_b200.h"
+
+namespace vgp {
+
+// ---------------------------------------------------------------- errors
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define VGP_CUDA_TRY(expr)                                                          \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return ::vgp::fail(VGP_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+constexpr double kLog2Pi = 1.8378770664093453;  // math.log(2*pi), vg/vecchia.py:31
+constexpr double kPi = 3.141592653589793;
+
+// Reduction chunk of vecchia._ordered_sum (vg/vecchia.py:35).
+constexpr int64_t kReduceChunk = 4096;
+
+// ---------------------------------------------------------------- covariance
+
+enum CovKind : int {
+  kMatern05 = 0,   // s2 exp(-u)                      vg/kernels.py:69-70
+  kMatern15 = 1,   // s2 (1+u) exp(-u)                vg/kernels.py:71-72
+  kMatern25 = 2,   // s2 (1+u+u^2/3) exp(-u)          vg/kernels.py:73-74
+  kMaternGen = 3,  // s2 2^(1-nu)/G(nu) u^nu K_nu(u)  vg/kernels.py:75-81
+  kPowExp = 4,     // s2 exp(-d^nu / beta)            vg/kernels.py:85-91
+};
+
+// Per-evaluation covariance constants (everything that depends on theta only
+// is folded on the host once per likelihood evaluation).
+struct CovParams {
+  int kind;
+  int nl;          // general nu: number of upward recurrence steps (nu = mu + nl)
+  double s2, beta, inv_beta, nu;
+  double coef;     // 2^(1-nu) / Gamma(nu)
+  double mu;       // nu - nl, in [-0.5, 0.5)
+  double gam1, gam2, gampl, gammi, fact;  // Temme series constants (see bessel_k)
+};
+
+int make_cov_params(int family, double s2, double beta, double nu, CovParams* out);
+
+// ---------------------------------------------------------------- plan
+
+struct Plan {
+  int device = 0;
+  int64_t n = 0;
+  int32_t m = 0;
+  int metric = VGP_METRIC_EUCLIDEAN;
+  double radius = 6371.0;
+  int64_t blk_lo = 0, blk_hi = 0;  // batch entries [blk_lo, blk_hi); entry 0 = joint block
+  int64_t rest_lo = 0, rest_hi = 0;  // block_rest indices k = e - 1 covered by this plan
+  cudaStream_t stream = nullptr;
+  int64_t* d_order = nullptr;   // n, ordered position -> original index
+  int32_t* d_nbr = nullptr;     // (rest_hi - rest_lo) x m, row r <-> entry rest_lo + r + 1
+  double4* d_pts = nullptr;     // n x (x, y, obs, 0), ordered
+  double* d_raw = nullptr;      // n x 3 upload staging (x, y, obs), original order
+  double* d_rest = nullptr;     // block_rest / mu_new / sigma_new for the local range
+  double* d_mu = nullptr;
+  double* d_sig = nullptr;
+  double* d_partials = nullptr; // chunk partials for local chunks
+  double* d_scalars = nullptr;  // [0] total, [1] block_first
+  unsigned long long* d_fail = nullptr;  // [0] NPD key, [1] variance index
+  double* d_work = nullptr;     // global workspace for the large-m generic path
+  size_t work_doubles = 0;
+  int work_slots = 0;
+  double* h_stage = nullptr;    // pinned host staging (n x 3 doubles)
+  double* h_small = nullptr;    // pinned scalars
+  bool has_data = false;
+  int num_sms = 148;
+  int64_t chunk_lo = 0, chunk_hi = 0;  // global 4096-chunk ids covered (rest range aligned)
+  int kernel_variant = -1;      // last kernel used (for introspection)
+  int force_variant = -1;       // -1 auto
+};
+
+// ---------------------------------------------------------------- kernels (launchers)
+
+// kNN, vg/geo.py:234-263 / :331-358. All pointers are device pointers.
+cudaError_t launch_knn(const double2* d_data, int64_t nd, const double2* d_query, int64_t nq,
+                       int64_t q_offset, int pred, int32_t m, int64_t* d_out, double* d_keys,
+                       int32_t* d_idx, cudaStream_t stream);
+
+// Permute raw (x, y, obs) rows into ordered double4 points.
+cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t n,
+                           double4* d_pts, cudaStream_t stream);
+
+// Generic per-block likelihood kernel (any m; smem- or global-resident block).
+cudaError_t launch_loglik_generic(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                                  cudaStream_t stream);
+
+// Fast warp-per-block DMMA kernel for m + 2 <= 64.  Returns cudaErrorNotSupported
+// when the shape is not covered.
+cudaError_t launch_loglik_dmma(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                               cudaStream_t stream);
+bool dmma_supported(int m, int kind);
+
+// numpy-pairwise 4096-chunk partials of d_rest and the ordered total.
+cudaError_t launch_reduce(const Plan& p, bool want_total, cudaStream_t stream);
+
+// Covariance evaluation at distances (kernels.cov, vg/kernels.py:94-98).
+cudaError_t launch_cov_eval(const CovParams& cp, const double* d_in, int64_t count, double* d_out,
+                            cudaStream_t stream);
+
+// K_nu(x) at given points (kernels.bessel_kv, vg/kernels.py:50-56); cp from
+// make_cov_params(MATERN, 1, 1, nu) with the general-nu constants filled.
+cudaError_t launch_bessel_eval(const CovParams& cp, const double* d_in, int64_t count,
+                               double* d_out, cudaStream_t stream);
+int make_bessel_params(double nu, CovParams* out);
+
+// NPD key: (chunk(e), pivot column, e) ordered like the reference's first raise
+// (vg/batchla.py:146-151 inside parallel.map_chunks, vg/parallel.py:37-43).
+__host__ __device__ inline unsigned long long npd_key(int64_t e, int j, int m) {
+  if (m > 256) return (unsigned long long)e;  // per-entry LAPACK path, vg/batchla.py:159-164
+  int64_t chunk = (int64_t(1) << 21) / (int64_t(m) * m);
+  if (chunk < 1) chunk = 1;
+  unsigned long long c = (unsigned long long)(e / chunk);
+  unsigned long long w = (unsigned long long)(e % chunk);
+  return (c << 42) | ((unsigned long long)j << 24) | w;
+}
+inline int64_t npd_key_entry(unsigned long long key, int m) {
+  if (m > 256) return (int64_t)key;
+  int64_t chunk = (int64_t(1) << 21) / (int64_t(m) * m);
+  if (chunk < 1) chunk = 1;
+  return (int64_t)(key >> 42) * chunk + (int64_t)(key & ((1ull << 24) - 1));
+}
+
+}  // namespace vgp

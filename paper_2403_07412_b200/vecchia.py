@@ -1,0 +1,296 @@
+"""Vecchia plans and the B200 log-likelihood (mirrors ``vecchiagp.vecchia``).
+
+``make_plan`` builds the ordering on the host and the conditioning sets on
+the GPU (``geo.nearest_neighbors``).  ``vecchia_loglik`` evaluates the
+ordered product of conditionals with one fused sm_100a kernel per call
+(gather -> Matérn generation -> POTRF/TRSV/dots -> per-block log-density)
+followed by the reference's deterministic 4096-chunk ordered reduction, so
+``total == block_first + _ordered_sum(block_rest)`` holds bit for bit
+(vg/vecchia.py:169-177, :213).
+
+Device state lives in :class:`DevicePlan` (a ``vgp_plan`` handle holding the
+permutation and the neighbour rows of a block range) cached on the plan
+object, and :class:`LikelihoodSession` (a DevicePlan with a resident
+dataset), which is what the MLE loop evaluates against.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import geo, kernels
+
+LOG_2PI = math.log(2.0 * math.pi)
+_REDUCE_CHUNK = 4096
+ORDERINGS = ("random", "morton", "identity")
+
+
+@dataclass
+class VecchiaPlan:
+    """Conditioning size, ordering, and neighbor table for one dataset (vg/vecchia.py:40-56)."""
+
+    m: int
+    permutation: geo.Permutation
+    neighbors: geo.NeighborTable
+    metric: geo.Metric
+    ordering: str = "custom"
+    _device_plans: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def __post_init__(self):
+        n = self.permutation.n
+        if self.m >= 1 and self.neighbors.neighbors.shape != (n - self.m, self.m):
+            raise ValueError(
+                f"neighbor table shape {self.neighbors.neighbors.shape} inconsistent "
+                f"with n={n}, m={self.m}"
+            )
+
+    def device_plan(self, device: int | None = None) -> "DevicePlan":
+        """Full-range device context on `device` (created once, then reused)."""
+        dev = N.current_device() if device is None else int(device)
+        dp = self._device_plans.get(dev)
+        if dp is None or dp.closed:
+            dp = DevicePlan(self, device=dev)
+            self._device_plans[dev] = dp
+        return dp
+
+
+def make_plan(dataset: geo.Dataset, m: int, ordering: str = "random", seed: int = 0) -> VecchiaPlan:
+    """Build the ordering and preceding-neighbor table for a dataset (vg/vecchia.py:59-82)."""
+    n = dataset.n
+    if ordering not in ORDERINGS:
+        raise ValueError(f"unknown ordering {ordering!r}; expected one of {ORDERINGS}")
+    if ordering == "random":
+        perm = geo.random_ordering(n, seed)
+    elif ordering == "morton":
+        perm = geo.morton_ordering(dataset.locations)
+    else:
+        perm = geo.Permutation(np.arange(n))
+    if n == 1:
+        table = geo.NeighborTable(m=0, neighbors=np.empty((0, 0), dtype=np.int64))
+        return VecchiaPlan(0, perm, table, dataset.metric, ordering)
+    if not (1 <= m < n):
+        raise ValueError(f"need 1 <= m < n, got m={m}, n={n}")
+    table = geo.nearest_neighbors(dataset.permute(perm), m)
+    return VecchiaPlan(m, perm, table, dataset.metric, ordering)
+
+
+@dataclass
+class LogLikResult:
+    """Total log-likelihood plus its per-block decomposition (vg/vecchia.py:95-103)."""
+
+    total: float
+    block_first: float
+    block_rest: np.ndarray
+    mu_new: np.ndarray
+    sigma_new: np.ndarray
+
+
+def _metric_code(metric) -> tuple[int, float]:
+    if isinstance(metric, geo.GreatCircle):
+        return N.METRIC_GREAT_CIRCLE, float(metric.radius)
+    return N.METRIC_EUCLIDEAN, geo.EARTH_RADIUS_KM
+
+
+def _release(handle: int) -> None:
+    if handle:
+        N.lib.vgp_plan_destroy(ctypes.c_void_p(handle))
+
+
+class DevicePlan:
+    """A ``vgp_plan``: permutation + neighbour rows of batch entries
+    [block_lo, block_hi) resident on one GPU (entry 0 = joint block)."""
+
+    def __init__(self, plan: VecchiaPlan, device: int | None = None, block_lo: int = 0,
+                 block_hi: int | None = None):
+        n = plan.permutation.n
+        m = plan.m
+        if not (1 <= m < n):
+            raise ValueError(f"need 1 <= m < n, got m={m}, n={n}")
+        count = n - m + 1
+        block_hi = count if block_hi is None else int(block_hi)
+        self.device = N.current_device() if device is None else int(device)
+        self.n, self.m = n, m
+        self.block_lo, self.block_hi = int(block_lo), block_hi
+        self.full = self.block_lo == 0 and self.block_hi == count
+        metric, radius = _metric_code(plan.metric)
+        order = np.ascontiguousarray(plan.permutation.order, dtype=np.int64)
+        table = np.ascontiguousarray(plan.neighbors.neighbors, dtype=np.int64)
+        h = ctypes.c_void_p()
+        N.check(N.lib.vgp_plan_create(self.device, n, m, metric, radius, N.iptr(order),
+                                      N.iptr(table), self.block_lo, self.block_hi, ctypes.byref(h)))
+        self._h = h
+        self._finalizer = weakref.finalize(self, _release, h.value)
+        info = self.info()
+        self.chunk_lo, self.nchunks = int(info[4]), int(info[5])
+        self._data_key = None
+
+    @property
+    def closed(self) -> bool:
+        return not self._finalizer.alive
+
+    def close(self) -> None:
+        self._finalizer()
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self.closed:
+            raise ValueError("device plan is closed")
+        return self._h
+
+    def info(self) -> np.ndarray:
+        out = np.zeros(8, dtype=np.int64)
+        N.check(N.lib.vgp_plan_info(self._h, N.iptr(out)))
+        return out
+
+    @property
+    def kernel_variant(self) -> int:
+        return int(self.info()[6])
+
+    def set_variant(self, variant: int) -> None:
+        """-1 auto, 0 generic kernel, 1 warp-DMMA kernel (testing aid)."""
+        N.check(N.lib.vgp_plan_set_variant(self.handle, int(variant)))
+
+    def set_data(self, dataset: geo.Dataset) -> None:
+        """Upload a dataset in original order; the device applies the permutation."""
+        if dataset.n != self.n:
+            raise ValueError(f"plan built for n={self.n}, dataset has n={dataset.n}")
+        locs = np.ascontiguousarray(dataset.locations, dtype=np.float64)
+        obs = np.ascontiguousarray(dataset.observations, dtype=np.float64)
+        N.check(N.lib.vgp_plan_set_data(self.handle, N.dptr(locs), N.dptr(obs)))
+
+    @property
+    def stream(self) -> int:
+        return int(N.lib.vgp_plan_stream(self.handle) or 0)
+
+    def loglik(self, spec: kernels.KernelSpec, full_result: bool = True) -> LogLikResult:
+        if not self.full:
+            raise ValueError("loglik needs a full-range plan; use partials() on shards")
+        p = spec.params
+        k = self.n - self.m
+        total = np.zeros(1)
+        bf = np.zeros(1)
+        fail = np.full(1, -1, dtype=np.int64)
+        if full_result:
+            rest, mu, sg = np.empty(k), np.empty(k), np.empty(k)
+            ptrs = (N.dptr(rest), N.dptr(mu), N.dptr(sg))
+        else:
+            rest = mu = sg = None
+            ptrs = (N.null_d(), N.null_d(), N.null_d())
+        rc = N.lib.vgp_loglik(self.handle, N.FAMILY_CODES[spec.family], float(p.sigma_sq),
+                              float(p.beta), float(p.nu), N.dptr(total), N.iptr(fail),
+                              N.dptr(bf), *ptrs)
+        N.raise_for_status(rc, int(fail[0]))
+        if not full_result:
+            rest = mu = sg = np.empty(0)
+        return LogLikResult(float(total[0]), float(bf[0]), rest, mu, sg)
+
+    def total(self, spec: kernels.KernelSpec) -> float:
+        return self.loglik(spec, full_result=False).total
+
+    def partials(self, spec: kernels.KernelSpec):
+        """(chunk partials, block_first, status, fail_index) of this shard."""
+        p = spec.params
+        parts = np.zeros(max(self.nchunks, 1))
+        bf = np.zeros(1)
+        fail = np.full(1, -1, dtype=np.int64)
+        rc = N.lib.vgp_loglik_partials(self.handle, N.FAMILY_CODES[spec.family], float(p.sigma_sq),
+                                       float(p.beta), float(p.nu), N.dptr(parts), N.dptr(bf),
+                                       N.iptr(fail))
+        N.check(rc)
+        return parts[: self.nchunks], float(bf[0]), int(rc), int(fail[0])
+
+    # -- launch-only interface for device-timed benchmarking
+    def launch(self, spec: kernels.KernelSpec) -> None:
+        p = spec.params
+        N.check(N.lib.vgp_loglik_async(self.handle, N.FAMILY_CODES[spec.family],
+                                       float(p.sigma_sq), float(p.beta), float(p.nu)))
+
+    def fetch(self):
+        total = np.zeros(1)
+        fail = np.full(1, -1, dtype=np.int64)
+        st = ctypes.c_int(0)
+        N.check(N.lib.vgp_plan_fetch(self.handle, N.dptr(total), N.iptr(fail), ctypes.byref(st)))
+        return float(total[0]), int(st.value), int(fail[0])
+
+
+class LikelihoodSession:
+    """A dataset resident on the GPU next to its plan: the MLE objective.
+
+    Equivalent to calling ``vecchia_loglik(dataset, plan, spec)`` repeatedly
+    with the same dataset, without re-uploading it each time.
+    """
+
+    def __init__(self, dataset: geo.Dataset, plan: VecchiaPlan, device: int | None = None):
+        if plan.permutation.n != dataset.n:
+            raise ValueError(f"plan built for n={plan.permutation.n}, dataset has n={dataset.n}")
+        self.dataset = dataset
+        self.plan = plan
+        self.single = dataset.n == 1
+        if not self.single:
+            self.dplan = DevicePlan(plan, device=device)
+            self.dplan.set_data(dataset)
+
+    def loglik(self, spec: kernels.KernelSpec) -> LogLikResult:
+        if self.single:
+            return _singleton(self.dataset, spec)
+        return self.dplan.loglik(spec)
+
+    def total(self, spec: kernels.KernelSpec) -> float:
+        if self.single:
+            return _singleton(self.dataset, spec).total
+        return self.dplan.total(spec)
+
+    def close(self) -> None:
+        if not self.single:
+            self.dplan.close()
+
+
+def _singleton(dataset: geo.Dataset, spec: kernels.KernelSpec) -> LogLikResult:
+    # exact univariate density for n == 1 (vg/vecchia.py:229-233)
+    s2 = spec.params.sigma_sq
+    y0 = float(dataset.observations[0])
+    ll = -0.5 * (y0 * y0 / s2 + LOG_2PI + math.log(s2))
+    return LogLikResult(ll, ll, np.empty(0), np.empty(0), np.empty(0))
+
+
+def vecchia_loglik(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.KernelSpec) -> LogLikResult:
+    """Vecchia-approximated Gaussian log-likelihood of a dataset (vg/vecchia.py:217-238).
+
+    The dataset (original order) is uploaded and permuted on the device each
+    call; the plan's permutation and neighbour table stay resident.  Raises
+    LikelihoodEvaluationError with the failing block index when a
+    conditioning matrix is not positive definite or a conditional variance is
+    non-positive.
+    """
+    if dataset.n == 1:
+        return _singleton(dataset, spec)
+    if plan.permutation.n != dataset.n:
+        raise ValueError(f"plan built for n={plan.permutation.n}, dataset has n={dataset.n}")
+    dp = plan.device_plan()
+    dp.set_data(dataset)
+    return dp.loglik(spec)
+
+
+def _ordered_sum(values: np.ndarray) -> float:
+    """4096-chunk pairwise partials combined in index order (vg/vecchia.py:169-177)."""
+    partials = [float(values[lo:lo + _REDUCE_CHUNK].sum())
+                for lo in range(0, values.shape[0], _REDUCE_CHUNK)]
+    total = 0.0
+    for p in partials:
+        total += p
+    return total
+
+
+def flop_count(n: int, m: int) -> float:
+    """(n - m + 1)(m^3/3 + 2 m^2 + 4 m), vg/vecchia.py:241-251."""
+    if not (1 <= m < n):
+        raise ValueError(f"need 1 <= m < n, got m={m}, n={n}")
+    blocks = float(n - m + 1)
+    fm = float(m)
+    return blocks * (fm**3 / 3.0 + 2.0 * fm**2 + 4.0 * fm)

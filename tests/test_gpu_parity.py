@@ -1,0 +1,266 @@
+"""GPU parity tests: the B200 path (through the C ABI via the package) against
+golden vectors produced by the reference itself (tests/golden/make_golden.py)
+and against the CPU oracle (oracle/) on identical seeded inputs.
+
+Tolerances (north star): log-likelihood totals relative <= 1e-9; neighbour
+tables bit-exact; covariance values relative <= 1e-12 (closed forms) and
+<= 1e-11 (general-nu Bessel path); MLE estimates relative <= 1e-4.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from _helpers import golden_names, load, rel
+
+pytestmark = pytest.mark.gpu
+
+TOL_TOTAL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def vg():
+    import paper_2403_07412_b200 as vg
+
+    if vg._native.device_count() == 0:
+        pytest.fail("GPU tests need a CUDA device: the B200 path has no CPU fallback")
+    return vg
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    from oracle import oracle as O
+
+    return O
+
+
+# ---------------------------------------------------------------- kNN
+
+@pytest.mark.parametrize("name", golden_names("knn_"))
+def test_knn_bit_exact_vs_reference(vg, name):
+    z = load(name)
+    m = int(z["m"])
+    if "query" in z.files:
+        got = vg.nearest_points(z["query"], z["train"], vg.Euclidean(), m)
+    else:
+        got = vg.nearest_neighbors(vg.Dataset(z["locs"], np.zeros(len(z["locs"]))), m).neighbors
+    assert got.dtype == np.int64
+    np.testing.assert_array_equal(got, z["table"])
+
+
+@pytest.mark.parametrize("n,m,seed", [(20000, 30, 0), (20000, 60, 1), (5000, 7, 2), (3000, 128, 3)])
+def test_knn_bit_exact_vs_oracle(vg, oracle, n, m, seed):
+    rng = np.random.default_rng(seed)
+    locs = rng.random((n, 2))
+    got = vg.nearest_neighbors(vg.Dataset(locs, np.zeros(n)), m).neighbors
+    np.testing.assert_array_equal(got, oracle.knn_pred(locs, m))
+
+
+def test_knn_ties_and_duplicates(vg, oracle):
+    rng = np.random.default_rng(7)
+    locs = rng.integers(0, 9, size=(2000, 2)).astype(np.float64) * 0.25
+    for m in (1, 5, 33):
+        got = vg.nearest_neighbors(vg.Dataset(locs, np.zeros(len(locs))), m).neighbors
+        np.testing.assert_array_equal(got, oracle.knn_pred(locs, m))
+
+
+def test_knn_points_vs_oracle(vg, oracle):
+    rng = np.random.default_rng(8)
+    train = rng.random((3000, 2))
+    query = rng.random((700, 2))
+    got = vg.nearest_points(query, train, vg.Euclidean(), 40)
+    np.testing.assert_array_equal(got, oracle.knn_points(query, train, 40))
+
+
+def test_c1_neighbor_table_digest(vg):
+    import hashlib
+
+    z = load("c1_n20000_m30_nu05")
+    locs = z["locs"][z["perm"]]
+    t = vg.nearest_neighbors(vg.Dataset(locs, np.zeros(len(locs))), 30).neighbors
+    assert hashlib.sha256(t.tobytes()).hexdigest() == str(z["table_sha256"])
+
+
+# ---------------------------------------------------------------- likelihood
+
+def _plan_from_golden(vg, z):
+    data = vg.Dataset(z["locs"], z["obs"])
+    perm = vg.Permutation(z["perm"])
+    table = vg.NeighborTable(int(z["m"]), z["table"])
+    plan = vg.VecchiaPlan(int(z["m"]), perm, table, vg.Euclidean(), str(z["ordering"]))
+    s2, beta, nu = (float(v) for v in z["theta"])
+    spec = vg.KernelSpec(str(z["family"]), vg.KernelParams(s2, beta, nu))
+    return data, plan, spec
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
+@pytest.mark.parametrize("variant", [-1, 0])
+def test_loglik_vs_reference_golden(vg, name, variant):
+    z = load(name)
+    data, plan, spec = _plan_from_golden(vg, z)
+    plan.device_plan().set_variant(variant)
+    res = vg.vecchia_loglik(data, plan, spec)
+    assert rel(res.total, float(z["total"])) <= TOL_TOTAL
+    assert rel(res.block_first, float(z["block_first"])) <= TOL_TOTAL
+    # per-block terms: ill-conditioned blocks amplify ulp-level differences
+    np.testing.assert_allclose(res.block_rest, z["block_rest"], rtol=1e-7, atol=1e-7)
+    np.testing.assert_allclose(res.mu_new, z["mu_new"], rtol=1e-7, atol=1e-7)
+    np.testing.assert_allclose(res.sigma_new, z["sigma_new"], rtol=1e-6, atol=1e-12)
+    # additivity as stored, bitwise (pkg/tests/test_vecchia.py:127-133)
+    assert res.total == res.block_first + vg.vecchia._ordered_sum(res.block_rest)
+    if "exact" in z.files:
+        assert rel(res.total, float(z["exact"])) <= 1e-8
+
+
+def test_loglik_failure_duplicate(vg):
+    z = load("ll_fail_duplicate")
+    data, plan, spec = _plan_from_golden(vg, z)
+    with pytest.raises(vg.LikelihoodEvaluationError) as err:
+        vg.vecchia_loglik(data, plan, spec)
+    assert err.value.block_index == int(z["fail_index"])
+
+
+def test_loglik_failure_npd_index(vg):
+    z = load("ll_fail_npd_dups")
+    data, plan, spec = _plan_from_golden(vg, z)
+    with pytest.raises(vg.LikelihoodEvaluationError) as err:
+        vg.vecchia_loglik(data, plan, spec)
+    assert err.value.block_index == int(z["fail_index"])
+
+
+def test_c1_loglik_and_blocks(vg):
+    z = load("c1_n20000_m30_nu05")
+    data = vg.Dataset(z["locs"], z["obs"])
+    plan = vg.make_plan(data, 30, "random", seed=0)
+    np.testing.assert_array_equal(plan.permutation.order, z["perm"])
+    spec = vg.KernelSpec("matern", vg.KernelParams(*[float(v) for v in z["theta"]]))
+    res = vg.vecchia_loglik(data, plan, spec)
+    assert rel(res.total, float(z["total"])) <= TOL_TOTAL
+    np.testing.assert_allclose(res.block_rest, z["block_rest"], rtol=1e-7, atol=1e-7)
+
+
+@pytest.mark.parametrize("n,m,nu,beta,seed", [
+    (30000, 60, 1.5, 0.052537, 11), (30000, 30, 0.5, 0.078809, 12), (20000, 45, 2.5, 0.03, 13),
+    (12000, 10, 1.5, 0.052537, 14), (8000, 62, 0.5, 0.1, 15), (6000, 96, 1.5, 0.05, 16),
+])
+def test_loglik_vs_oracle_seeded(vg, oracle, n, m, nu, beta, seed):
+    """Model-consistent y (Vecchia forward simulation under the same theta,
+    SURVEY.md §7 H5); totals must agree at 1e-9."""
+    rng = np.random.default_rng(seed)
+    locs = rng.random((n, 2))
+    data = vg.Dataset(locs, np.zeros(n))
+    plan = vg.make_plan(data, m, "random", seed=seed)
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, beta, nu))
+    y_ord = oracle.simulate_vecchia(locs[plan.permutation.order], m, plan.neighbors.neighbors,
+                                    "matern", 1.0, beta, nu, seed + 100)
+    y = np.empty(n)
+    y[plan.permutation.order] = y_ord
+    data = vg.Dataset(locs, y)
+    ordered = data.permute(plan.permutation)
+    ref = oracle.loglik(ordered.locations, ordered.observations, m, plan.neighbors.neighbors,
+                        "matern", 1.0, beta, nu)
+    res = vg.vecchia_loglik(data, plan, spec)
+    assert ref.status == 0
+    assert rel(res.total, ref.total) <= TOL_TOTAL
+
+
+def test_singleton_exact_convention(vg):
+    spec = vg.KernelSpec("matern", vg.KernelParams(2.0, 0.1, 0.5))
+    data = vg.Dataset(np.array([[0.5, 0.5]]), np.array([1.3]))
+    plan = vg.make_plan(data, m=1, ordering="identity")
+    res = vg.vecchia_loglik(data, plan, spec)
+    expected = -0.5 * (1.3**2 / 2.0 + math.log(2 * math.pi) + math.log(2.0))
+    assert res.total == pytest.approx(expected, rel=1e-15)
+    assert res.block_rest.size == 0
+
+
+def test_bivariate_closed_form(vg):
+    d, y1, y2 = 0.37, 0.8, -0.45
+    data = vg.Dataset(np.array([[0.0, 0.0], [d, 0.0]]), np.array([y1, y2]))
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, 1.0, 0.5))
+    plan = vg.make_plan(data, 1, "identity")
+    res = vg.vecchia_loglik(data, plan, spec)
+    rho = math.exp(-d)
+    first = -0.5 * (y1**2 + math.log(2 * math.pi))
+    cvar = 1.0 - rho**2
+    second = -0.5 * ((y2 - rho * y1) ** 2 / cvar + math.log(2 * math.pi) + math.log(cvar))
+    assert res.block_first == pytest.approx(first, rel=1e-14)
+    assert res.total == pytest.approx(first + second, rel=1e-14)
+
+
+def test_deterministic_repeat(vg):
+    z = load("ll_n3000_m60_nu15")
+    data, plan, spec = _plan_from_golden(vg, z)
+    a = vg.vecchia_loglik(data, plan, spec)
+    b = vg.vecchia_loglik(data, plan, spec)
+    assert a.total == b.total
+    np.testing.assert_array_equal(a.block_rest, b.block_rest)
+
+
+# ---------------------------------------------------------------- kernels
+
+@pytest.mark.parametrize("nu", [0.5, 1.5, 2.5, 0.05, 0.3, 0.8, 1.0, 1.2, 2.3, 3.7, 5.0])
+def test_cov_matches_scipy_reference_formula(vg, oracle, nu):
+    d = np.concatenate([[0.0], np.geomspace(1e-8, 80.0, 400)])
+    for fam in ("matern", "power_exponential"):
+        p = vg.KernelParams(1.7, 0.13, nu if fam == "matern" else min(nu, 2.0))
+        got = vg.kernels.cov(d, vg.KernelSpec(fam, p))
+        want = oracle.cov(d, fam, p.sigma_sq, p.beta, p.nu)
+        tol = 1e-12 if (fam != "matern" or nu in (0.5, 1.5, 2.5)) else 1e-11
+        scale = np.maximum(np.abs(want), 1e-300)
+        assert np.max(np.abs(got - want) / scale) <= tol, (fam, nu)
+
+
+@pytest.mark.parametrize("nu", [0.0, 0.1, 0.5, 0.9, 1.5, 2.0, 2.5, 3.3, 4.9])
+def test_bessel_kv_vs_scipy(vg, nu):
+    from scipy.special import kv
+
+    x = np.geomspace(1e-6, 650.0, 500)
+    got = vg.bessel_kv(nu, x)
+    want = kv(nu, x)
+    assert np.max(np.abs(got - want) / want) <= 1e-12
+
+
+# ---------------------------------------------------------------- batched LA
+
+def test_batch_ops_match_oracle(vg, oracle):
+    rng = np.random.default_rng(3)
+    count, dim = 300, 17
+    a = rng.standard_normal((count, dim, dim))
+    spd = a @ np.transpose(a, (0, 2, 1)) + dim * np.eye(dim)
+    batch = vg.StridedMatrixBatch.from_matrices(spd)
+    vg.batch_potrf(batch)
+    ref = spd.copy()
+    assert oracle._potrf_sweep(ref) is None
+    np.testing.assert_allclose(np.tril(batch.mats), np.tril(ref), rtol=1e-13, atol=1e-13)
+    b = vg.StridedVectorBatch.from_vectors(rng.standard_normal((count, dim)))
+    x = vg.batch_trsv(batch, b)
+    np.testing.assert_allclose(x.vecs, oracle._trsv(ref, b.vecs.copy()), rtol=1e-12, atol=1e-12)
+    d = vg.batch_dot(x, b)
+    np.testing.assert_array_equal(d.values, oracle._dot(x.vecs, b.vecs))
+
+
+def test_batch_potrf_npd_index(vg):
+    mats = np.stack([np.eye(4)] * 5)
+    mats[3, 2, 2] = -1.0
+    with pytest.raises(vg.NonPositiveDefiniteError) as err:
+        vg.batch_potrf(vg.StridedMatrixBatch.from_matrices(mats))
+    assert err.value.batch_index == 3
+
+
+# ---------------------------------------------------------------- MLE
+
+def test_c1_mle_matches_reference(vg):
+    z = load("c1_n20000_m30_nu05")
+    if "mle_theta" not in z.files:
+        pytest.skip("golden file generated without --with-mle")
+    data = vg.Dataset(z["locs"], z["obs"])
+    cfg = vg.FitConfig(objective="vecchia", m=30, ordering="random", seed=0,
+                       init=vg.KernelParams(0.5, 0.05, 0.5))
+    fr = vg.mle_estimate(data, cfg)
+    th = z["mle_theta"]
+    assert rel(fr.theta_hat.sigma_sq, float(th[0])) <= 1e-4
+    assert rel(fr.theta_hat.beta, float(th[1])) <= 1e-4
+    assert fr.theta_hat.nu == 0.5
+    assert rel(fr.loglik, float(z["mle_loglik"])) <= 1e-9
