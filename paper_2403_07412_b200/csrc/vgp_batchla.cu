@@ -4,7 +4,7 @@
 // the reference's phase-split bench, vg/cli.py:257-270).  Layout: matrix k
 // at buffer + k*stride, column-major, entry (i, j) at j*dim + i
 // (vg/batchla.py:74-82).  Arithmetic follows the reference sweep (true
-// divisions, ascending dots).
+// divisions, separately rounded products and sums, ascending dots).
 #include <algorithm>
 #include <string>
 
@@ -42,7 +42,8 @@ potrf_kernel(double* __restrict__ buf, int64_t count, int dim, int64_t stride,
       __syncthreads();
       for (int i = j + 1 + threadIdx.x; i < dim; i += blockDim.x) {
         const double lij = A[i + (int64_t)j * dim];
-        for (int c = j + 1; c <= i; ++c) A[i + (int64_t)c * dim] -= lij * A[c + (int64_t)j * dim];
+        for (int c = j + 1; c <= i; ++c)
+          A[i + (int64_t)c * dim] = __dsub_rn(A[i + (int64_t)c * dim], __dmul_rn(lij, A[c + (int64_t)j * dim]));
       }
       __syncthreads();
     }
@@ -69,7 +70,7 @@ __global__ void trsv_kernel(const double* __restrict__ L, int64_t lstride, const
     }
     double xj = xs[j] / piv;
     xs[j] = xj;
-    for (int i = j + 1; i < dim; ++i) xs[i] -= A[i + (int64_t)j * dim] * xj;
+    for (int i = j + 1; i < dim; ++i) xs[i] = __dsub_rn(xs[i], __dmul_rn(A[i + (int64_t)j * dim], xj));
   }
 }
 
@@ -79,7 +80,7 @@ __global__ void dot_kernel(const double* __restrict__ a, const double* __restric
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   double acc = 0.0;
-  for (int i = 0; i < dim; ++i) acc += a[k * stride + i] * b[k * stride + i];
+  for (int i = 0; i < dim; ++i) acc = __dadd_rn(acc, __dmul_rn(a[k * stride + i], b[k * stride + i]));
   out[k] = acc;
 }
 

@@ -106,7 +106,8 @@ loglik_generic_kernel(const double4* __restrict__ pts, const int32_t* __restrict
       for (int i = j + 1 + threadIdx.x; i < P; i += blockDim.x) {
         const double lij = A[i + (size_t)j * ld];
         const int kmax = i < m ? i : m - 1;
-        for (int k = j + 1; k <= kmax; ++k) A[i + (size_t)k * ld] -= lij * A[k + (size_t)j * ld];
+        for (int k = j + 1; k <= kmax; ++k)
+          A[i + (size_t)k * ld] = __dsub_rn(A[i + (size_t)k * ld], __dmul_rn(lij, A[k + (size_t)j * ld]));
       }
       __syncthreads();
     }
@@ -121,8 +122,8 @@ loglik_generic_kernel(const double4* __restrict__ pts, const int32_t* __restrict
       for (int k = 0; k < m; ++k) {
         double vk = A[m + (size_t)k * ld];
         double yk = A[m + 1 + (size_t)k * ld];
-        accm += yk * vk;
-        accs += vk * vk;
+        accm = __dadd_rn(accm, __dmul_rn(yk, vk));  // no contraction: numpy rounds each op
+        accs = __dadd_rn(accs, __dmul_rn(vk, vk));
       }
       if (joint) {
         // block_first = -half_log_det(L0) - mu'0/2 - (m/2) log 2pi, vg/vecchia.py:202-204
