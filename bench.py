@@ -1,0 +1,408 @@
+"""Benchmark: Vecchia log-likelihood evaluations per second (BASELINE.json).
+
+Workload (BASELINE config 2): n = 1,000,000 uniform locations in [0,1]^2,
+m = 60, random ordering (seed 0), Matérn nu = 1.5, sigma^2 = 1,
+beta = 0.052537 (vg/kernels.py:118), FP64.  One "step" = one full
+log-likelihood evaluation (all n - m + 1 blocks, fused kernel + ordered
+reduction) of the same plan.  Inputs (32 MB points + 240 MB int32 neighbour
+table) exceed the 126 MB L2, so no explicit flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: blocks are sharded in fixed
+4096-entry chunks and one NCCL all-reduce per evaluation combines the
+partials (strong scaling: the problem size is fixed).
+
+`--impl reference` times the reference algorithm's CPU implementation on the
+host cores: the C restatement under oracle/ (the reference itself is Python
+and does not travel to the GPU box), on a prefix sample of the same ordered
+problem, extrapolated per block (time is linear in n, reference acceptance
+criterion C8).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.jsonl)
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA.8x8x4, 148 SMs @1965 MHz (profiles/r01_fp64_peak.jsonl)"
+KERNELS_PER_EVAL = 4  # joint block, fused block kernel, chunk partials, ordered total
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--m", type=int, default=60)
+    ap.add_argument("--nu", type=float, default=1.5)
+    ap.add_argument("--beta", type=float, default=0.052537)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def synthetic(n, seed=0):
+    rng = np.random.default_rng(seed)
+    locs = rng.random((n, 2))
+    # timing only needs a finite field (as the reference's own bench, vg/cli.py:245-250)
+    y = rng.standard_normal(n)
+    return locs, y
+
+
+def workload(args):
+    return {"workload": "vecchia_loglik", "n": args.n, "m": args.m, "kernel": "matern",
+            "nu": args.nu, "sigma_sq": 1.0, "beta": args.beta, "ordering": "random(seed=0)",
+            "locations": "U[0,1]^2 seed 0", "l2": "inputs > L2 (272 MB), no flush"}
+
+
+def flop_count(n, m):
+    return float(n - m + 1) * (m**3 / 3.0 + 2.0 * m**2 + 4.0 * m)
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU baseline
+
+def cpu_baseline(args, locs_ordered, y_ordered, table, threads=None):
+    """Oracle C restatement (oracle/vecchia_oracle.c) on a prefix of the same
+    ordered problem: the first n' ordered points form exactly the first
+    n' - m + 1 blocks.  Returns (evals/s extrapolated, sample description,
+    seconds, threads)."""
+    from oracle import oracle as O
+
+    threads = threads or (os.cpu_count() or 1)
+    m = args.m
+
+    def run(nn):
+        t0 = time.perf_counter()
+        r = O.loglik(locs_ordered[:nn], y_ordered[:nn], m, table[: nn - m], "matern", 1.0,
+                     args.beta, args.nu, threads=threads)
+        dt = time.perf_counter() - t0
+        if r.status != 0:
+            raise RuntimeError(f"oracle evaluation failed: status {r.status}")
+        return dt
+
+    n_cal = min(args.n, 20000)
+    t_cal = run(n_cal)
+    blocks_cal = n_cal - m + 1
+    per_block = t_cal / blocks_cal
+    n_s = int(min(args.n, max(n_cal, args.cpu_seconds / per_block + m - 1)))
+    t_s = run(n_s) if n_s > n_cal else t_cal
+    blocks_s = n_s - m + 1
+    sec_per_eval = t_s / blocks_s * (args.n - m + 1)
+    sample = (f"prefix n'={n_s} of the ordered problem ({blocks_s} of {args.n - m + 1} blocks, "
+              f"{t_s:.1f}s), extrapolated per block")
+    return 1.0 / sec_per_eval, sample, t_s, threads
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args, rank, world):
+    """`--impl reference`: the reference algorithm on host cores (oracle port)."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    locs, y = synthetic(args.n)
+    perm = np.random.default_rng(0).permutation(args.n)
+    ol, oy = locs[perm], y[perm]
+    # the reference's own (CPU) conditioning-set search on the prefix actually timed
+    threads = os.cpu_count() or 1
+    m = args.m
+    t0 = time.perf_counter()
+    n_cal = min(args.n, 20000)
+    table_cal = O.knn_pred(ol[:n_cal], m, threads)
+    r = O.loglik(ol[:n_cal], oy[:n_cal], m, table_cal, "matern", 1.0, args.beta, args.nu, threads)
+    per_block = (time.perf_counter() - t0) / (n_cal - m + 1)
+    budget = max(2.0, min(15.0, 120.0 / max(1, args.steps + args.warmup)))
+    n_s = int(min(args.n, max(n_cal, budget / per_block)))
+    table = O.knn_pred(ol[:n_s], m, threads)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = O.loglik(ol[:n_s], oy[:n_s], m, table, "matern", 1.0, args.beta, args.nu, threads)
+        dt = time.perf_counter() - t0
+        if r.status != 0:
+            raise RuntimeError("reference evaluation failed")
+        if i >= args.warmup:
+            times.append(dt)
+    blocks_s = n_s - m + 1
+    sec_per_eval = statistics.mean(times) / blocks_s * (args.n - m + 1)
+    value = 1.0 / sec_per_eval
+    sample = (f"prefix n'={n_s} of the ordered c2 problem ({blocks_s} blocks per step), "
+              f"extrapolated per block to n={args.n}")
+    line = {
+        "impl": "reference", "metric": "vecchia_loglik_evals_per_s", "value": value,
+        "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * sec_per_eval, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours_single(args):
+    import torch
+
+    import paper_2403_07412_b200 as vg
+
+    dev = 0
+    vg._native.set_device(dev)
+    torch.cuda.set_device(dev)
+    locs, y = synthetic(args.n)
+    data = vg.Dataset(locs, y)
+    t0 = time.perf_counter()
+    plan = vg.make_plan(data, args.m, "random", seed=0)
+    knn_s = time.perf_counter() - t0
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, args.beta, args.nu))
+    dp = plan.device_plan(dev)
+    dp.set_data(data)
+    stream = torch.cuda.ExternalStream(dp.stream)
+
+    for _ in range(args.warmup):
+        dp.launch(spec)
+    total, st, _ = dp.fetch()
+    if st != 0:
+        raise RuntimeError(f"evaluation failed with status {st}")
+
+    dp.set_timing(True)
+    dp.kernel_time()  # reset
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            dp.launch(spec)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    k_ms, k_launches = dp.kernel_time()
+    dp.set_timing(False)
+    total2, st2, _ = dp.fetch()
+    if st2 != 0 or total2 != total:
+        raise RuntimeError("non-deterministic or failed evaluation in the timed region")
+    k_avg_ms = k_ms / max(k_launches, 1)
+
+    # e2e: the public drop-in call with host buffers (upload + full LogLikResult back)
+    for _ in range(1):
+        vg.vecchia_loglik(data, plan, spec)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        res = vg.vecchia_loglik(data, plan, spec)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if res.total != total:
+        raise RuntimeError("e2e total differs from device-resident total")
+    h2d = args.n * 16 + args.n * 8
+    d2h = 3 * (args.n - args.m) * 8 + 24
+
+    flops = flop_count(args.n, args.m)
+    achieved = flops / (k_avg_ms * 1e-3) / 1e12
+    line = {
+        "metric": "vecchia_loglik_evals_per_s", "value": 1000.0 / ms, "unit": "evals/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload(args),
+        "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA + DFMA)", "achieved": achieved,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(),
+                     "peak_source": FP64_PEAK_SOURCE,
+                     "algorithmic": "flop_count(n,m)=(n-m+1)(m^3/3+2m^2+4m) per launch "
+                                    "(vg/vecchia.py:241-251), covariance generation excluded",
+                     "kernel_ms": k_avg_ms, "kernel_share": k_avg_ms / ms},
+        "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "api": "paper_2403_07412_b200.vecchia_loglik(dataset, plan, spec)"},
+        "gpu_launches": KERNELS_PER_EVAL * args.steps,
+        "clocks": clk.summary(),
+        "knn_s": knn_s, "total": total,
+        "kernel_variant": "warp-dmma" if dp.kernel_variant == 1 else "generic",
+    }
+    if not args.no_cpu_baseline:
+        ordered = data.permute(plan.permutation)
+        v, sample, secs, threads = cpu_baseline(args, ordered.locations, ordered.observations,
+                                                plan.neighbors.neighbors)
+        line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": threads, "kind": "port",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours_multi(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_07412_b200 as vg
+    from paper_2403_07412_b200.distributed import ShardedVecchia
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    vg._native.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    locs, y = synthetic(args.n)
+    data = vg.Dataset(locs, y)
+    t0 = time.perf_counter()
+    plan = vg.make_plan(data, args.m, "random", seed=0)
+    knn_s = time.perf_counter() - t0
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, args.beta, args.nu))
+    sh = ShardedVecchia(data, plan, device=local)
+    for _ in range(args.warmup):
+        total = sh.total(spec)
+    if sh.dplan is not None:
+        sh.dplan.set_timing(True)
+        sh.dplan.kernel_time()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            t = sh.total(spec)
+        ev1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    k_ms, k_n = sh.dplan.kernel_time() if sh.dplan is not None else (0.0, 0)
+    mx = torch.tensor([ms_local, k_ms / max(k_n, 1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    ms, k_avg_ms = (float(v) for v in mx.cpu().tolist())
+    if t != total:
+        raise RuntimeError("non-deterministic sharded total")
+    # e2e: dataset re-upload + sharded evaluation through the public API
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        sh.set_data(data)
+        sh.total(spec)
+    e2e_local = (time.perf_counter() - t0) / args.e2e_steps
+    e2e_t = torch.tensor([e2e_local], dtype=torch.float64, device="cuda")
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    if rank == 0:
+        nshard = max(1, sh.block_hi - sh.block_lo)
+        flops_rank = flop_count(args.n, args.m) * nshard / (args.n - args.m + 1)
+        achieved = flops_rank / (k_avg_ms * 1e-3) / 1e12
+        line = {
+            "metric": "vecchia_loglik_evals_per_s", "value": 1000.0 / ms, "unit": "evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": dict(workload(args), parallelism=f"blocks{world}"),
+            "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA + DFMA)", "achieved": achieved,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(),
+                         "peak_source": FP64_PEAK_SOURCE, "kernel_ms": k_avg_ms,
+                         "note": "rank-0 shard kernel, max over ranks"},
+            "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s",
+                    "h2d_bytes_per_step": args.n * 24, "d2h_bytes_per_step": 8 * (sh.buf.numel()),
+                    "api": "paper_2403_07412_b200.distributed.ShardedVecchia"},
+            "gpu_launches": (KERNELS_PER_EVAL + 1) * args.steps,
+            "clocks": clk.summary(), "knn_s": knn_s, "total": total,
+            "collective": "1 NCCL all_reduce(SUM) of 1+n_chunks fp64 per eval",
+        }
+        print(json.dumps(line), flush=True)
+    sh.close()
+    dist.destroy_process_group()
+
+
+def ncu_traffic():
+    """dram bytes per launch of the fused kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_fused_kernel.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        run_ours_multi(args, rank, world)
+    else:
+        run_ours_single(args)
+
+
+if __name__ == "__main__":
+    main()

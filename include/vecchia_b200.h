@@ -129,6 +129,22 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
 int vgp_loglik_partials(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
                         double* partials, double* block_first, int64_t* fail_index);
 
+/* Device form of vgp_loglik_partials for the NCCL path: launches the shard's
+ * evaluation on the plan's stream and writes into the DEVICE vector `out`
+ * (length 1 + total chunk count, zero-initialised by the caller):
+ * out[0] = block_first (plan holding entry 0 only), out[1 + c] = partial of
+ * global chunk c for the plan's chunks.  A failed shard writes NaN into its
+ * first slot so the all-reduced total is NaN; the exact failing index is then
+ * available from vgp_plan_fetch.  Synchronises the stream before returning. */
+int vgp_loglik_partials_device(vgp_plan* plan, int family, double sigma_sq, double beta,
+                               double nu, double* out);
+
+/* Per-kernel timing of the fused block kernel (CUDA events on the plan's
+ * stream around every launch while enabled).  vgp_plan_kernel_time returns
+ * the summed milliseconds and launch count since the last call and resets. */
+int vgp_plan_set_timing(vgp_plan* plan, int enable);
+int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches);
+
 /* Plan geometry: info[0] = n, [1] = m, [2] = block_lo, [3] = block_hi,
  * [4] = first global chunk, [5] = chunk count, [6] = last kernel variant
  * (0 generic, 1 warp-DMMA), [7] = device. */

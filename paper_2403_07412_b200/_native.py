@@ -41,7 +41,8 @@ EXPORTS = (
     "vgp_knn_points", "vgp_cov", "vgp_bessel_kv", "vgp_plan_create", "vgp_plan_set_data",
     "vgp_plan_destroy", "vgp_loglik", "vgp_loglik_partials", "vgp_plan_info",
     "vgp_plan_set_variant", "vgp_plan_stream", "vgp_loglik_async", "vgp_plan_fetch",
-    "vgp_batch_potrf", "vgp_batch_trsv", "vgp_batch_dot",
+    "vgp_batch_potrf", "vgp_batch_trsv", "vgp_batch_dot", "vgp_loglik_partials_device",
+    "vgp_plan_set_timing", "vgp_plan_kernel_time",
 )
 
 
@@ -95,6 +96,9 @@ _sig("vgp_plan_set_variant", _int, [_vp, _int])
 _sig("vgp_plan_stream", _vp, [_vp])
 _sig("vgp_loglik_async", _int, [_vp, _int, _d, _d, _d])
 _sig("vgp_plan_fetch", _int, [_vp, _dp, _ip, ctypes.POINTER(_int)])
+_sig("vgp_loglik_partials_device", _int, [_vp, _int, _d, _d, _d, _vp])
+_sig("vgp_plan_set_timing", _int, [_vp, _int])
+_sig("vgp_plan_kernel_time", _int, [_vp, _dp, _ip])
 _sig("vgp_batch_potrf", _int, [_int, _dp, _i64, _i32, _i64, _ip])
 _sig("vgp_batch_trsv", _int, [_int, _dp, _i64, _dp, _dp, _i64, _i32, _i64, _ip])
 _sig("vgp_batch_dot", _int, [_int, _dp, _dp, _i64, _i32, _i64, _dp])

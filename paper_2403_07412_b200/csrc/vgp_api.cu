@@ -147,8 +147,29 @@ void free_plan(Plan* p) {
   cudaFree(p->d_work);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->h_small) cudaFreeHost(p->h_small);
+  if (p->events) {
+    for (auto& pr : *p->events) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    delete p->events;
+  }
+  if (p->event_pool) {
+    for (auto ev : *p->event_pool) cudaEventDestroy(ev);
+    delete p->event_pool;
+  }
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
+}
+
+int take_event(Plan* p, cudaEvent_t* ev) {
+  if (!p->event_pool->empty()) {
+    *ev = p->event_pool->back();
+    p->event_pool->pop_back();
+    return VGP_OK;
+  }
+  VGP_CUDA_TRY(cudaEventCreate(ev));
+  return VGP_OK;
 }
 
 // Launch the full evaluation sequence on the plan's stream.
@@ -167,12 +188,23 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
     if (p->force_variant == 0) use_dmma = false;
     if (p->force_variant == 1 && !use_dmma)
       return fail(VGP_E_UNSUPPORTED, "warp-DMMA variant does not cover this m / kernel");
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (p->timing) {
+      int rc = take_event(p, &ev0);
+      if (!rc) rc = take_event(p, &ev1);
+      if (rc) return rc;
+      VGP_CUDA_TRY(cudaEventRecord(ev0, s));
+    }
     if (use_dmma) {
       VGP_CUDA_TRY(launch_loglik_dmma(*p, cp, e_lo, e_hi, s));
       p->kernel_variant = 1;
     } else {
       VGP_CUDA_TRY(launch_loglik_generic(*p, cp, e_lo, e_hi, s));
       p->kernel_variant = 0;
+    }
+    if (p->timing) {
+      VGP_CUDA_TRY(cudaEventRecord(ev1, s));
+      p->events->emplace_back(ev0, ev1);
     }
   }
   VGP_CUDA_TRY(launch_reduce(*p, want_total, s));
@@ -380,6 +412,8 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
   p->chunk_lo = rest_lo / kReduceChunk;
   p->chunk_hi = (p->rest_hi + kReduceChunk - 1) / kReduceChunk;
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  p->events = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
+  p->event_pool = new std::vector<cudaEvent_t>();
   const int64_t nrest = p->rest_hi - p->rest_lo;
   cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
@@ -480,6 +514,49 @@ int vgp_plan_info(const vgp_plan* plan, int64_t* info) {
   info[5] = p.chunk_hi - p.chunk_lo;
   info[6] = p.kernel_variant;
   info[7] = p.device;
+  return VGP_OK;
+}
+
+int vgp_loglik_partials_device(vgp_plan* plan, int family, double sigma_sq, double beta,
+                               double nu, double* out) {
+  if (!plan || !out) return fail(VGP_E_INVALID, "null pointer");
+  Plan* p = &plan->p;
+  if (!p->has_data) return fail(VGP_E_INVALID, "plan has no data (vgp_plan_set_data)");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  DeviceGuard g(p->device);
+  rc = launch_eval(p, cp, false);
+  if (rc) return rc;
+  VGP_CUDA_TRY(launch_scatter_partials(*p, out, p->stream));
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return VGP_OK;
+}
+
+int vgp_plan_set_timing(vgp_plan* plan, int enable) {
+  if (!plan) return fail(VGP_E_INVALID, "null plan");
+  plan->p.timing = enable != 0;
+  return VGP_OK;
+}
+
+int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
+  if (!plan) return fail(VGP_E_INVALID, "null plan");
+  Plan* p = &plan->p;
+  DeviceGuard g(p->device);
+  double total = 0.0;
+  int64_t count = 0;
+  for (auto& pr : *p->events) {
+    VGP_CUDA_TRY(cudaEventSynchronize(pr.second));
+    float t = 0.f;
+    VGP_CUDA_TRY(cudaEventElapsedTime(&t, pr.first, pr.second));
+    total += t;
+    ++count;
+    p->event_pool->push_back(pr.first);
+    p->event_pool->push_back(pr.second);
+  }
+  p->events->clear();
+  if (ms) *ms = total;
+  if (launches) *launches = count;
   return VGP_OK;
 }
 

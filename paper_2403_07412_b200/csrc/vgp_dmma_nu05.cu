@@ -1,0 +1,10 @@
+// Instantiation of the warp-DMMA kernel for kMatern05 (split per smoothness so the
+// large unrolled kernels compile in parallel).
+#include "vgp_dmma_kernel.cuh"
+
+namespace vgp {
+cudaError_t launch_dmma_kMatern05(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                                cudaStream_t stream) {
+  return dmma::launch_kind<kMatern05>(p, cp, e_lo, e_hi, stream);
+}
+}  // namespace vgp

@@ -1,0 +1,63 @@
+// Lean FP64 math for the fused covariance generation.  Every routine is
+// within ~2 ulp of the correctly rounded value over the domain the kernel
+// uses (checked against numpy in tests/test_gpu_kernels.py), has no
+// special-case branches, and spends at most a third of libdevice's FP64
+// instructions:
+//   sqrt_pos      MUFU.RSQ64H seed + two Newton steps on the root    6 FP64
+//   rsqrt_pos     MUFU.RSQ64H seed + two Newton steps                 8 FP64
+//   exp_neg_tab   exp(-u) = T[j] * p(r) * 2^e, 256-entry 2^(j/256)
+//                 table, Cody-Waite reduction, degree-4 polynomial     9 FP64
+#pragma once
+
+#include "vgp_exp_table.cuh"
+
+namespace vgp {
+
+__device__ __forceinline__ double rsqrt_seed(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// sqrt(x) for x >= 0; x below the normal range (duplicate points) gives 0.
+__device__ __forceinline__ double sqrt_pos(double x) {
+  const double y = rsqrt_seed(x);
+  const double h = 0.5 * y;
+  double s = x * y;
+  double r = fma(-s, s, x);
+  s = fma(r, h, s);
+  r = fma(-s, s, x);
+  s = fma(r, h, s);
+  return (__double2hiint(x) < 0x00100000) ? 0.0 : s;
+}
+
+// 1/sqrt(x) for normal x > 0.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y = rsqrt_seed(x);
+  double e = fma(-(x * y), y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-(x * y), y, 1.0);
+  y = fma(0.5 * y, e, y);
+  return y;
+}
+
+// tab[j] = scale * 2^(j/256) (shared memory).  Returns scale * exp(-u) for
+// u >= 0, and 0 once the result would leave the normal range (u > 690).
+__device__ __forceinline__ double exp_neg_tab(double u, const double* __restrict__ tab) {
+  const double shift = 0x1.8p52;
+  const double t = fma(-u, k256OverLn2, shift);  // round(-u * 256 / ln 2) in the low word
+  const double kf = t - shift;
+  const int ki = __double2loint(t);
+  double r = fma(-kf, kLn2Over256Hi, -u);
+  r = fma(-kf, kLn2Over256Lo, r);
+  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double v = tab[ki & 255] * p;
+  const int e = ki >> 8;  // arithmetic shift: floor(k / 256)
+  const double out = __hiloint2double(__double2hiint(v) + (e << 20), __double2loint(v));
+  return (ki < -254000) ? 0.0 : out;  // integer test: u > ~688
+}
+
+}  // namespace vgp

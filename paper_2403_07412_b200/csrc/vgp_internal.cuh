@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "vecchia_b200.h"
 
@@ -83,6 +85,9 @@ struct Plan {
   int64_t chunk_lo = 0, chunk_hi = 0;  // global 4096-chunk ids covered (rest range aligned)
   int kernel_variant = -1;      // last kernel used (for introspection)
   int force_variant = -1;       // -1 auto
+  bool timing = false;          // record events around the fused kernel
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* events = nullptr;  // pending pairs
+  std::vector<cudaEvent_t>* event_pool = nullptr;
 };
 
 // ---------------------------------------------------------------- kernels (launchers)
@@ -105,6 +110,10 @@ cudaError_t launch_loglik_generic(const Plan& p, const CovParams& cp, int64_t e_
 cudaError_t launch_loglik_dmma(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                                cudaStream_t stream);
 bool dmma_supported(int m, int kind);
+
+// Scatter the shard's chunk partials (and block_first) into a global device
+// vector for the cross-GPU all-reduce; NaN-poison on failure.
+cudaError_t launch_scatter_partials(const Plan& p, double* d_out, cudaStream_t stream);
 
 // numpy-pairwise 4096-chunk partials of d_rest and the ordered total.
 cudaError_t launch_reduce(const Plan& p, bool want_total, cudaStream_t stream);

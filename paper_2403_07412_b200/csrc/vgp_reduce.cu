@@ -63,6 +63,22 @@ __global__ void total_kernel(const double* __restrict__ partials, int64_t nchunk
   scalars[0] = scalars[1] + s;
 }
 
+__global__ void scatter_partials_kernel(const double* __restrict__ partials, int64_t nch,
+                                        int64_t chunk_lo, int has_first,
+                                        const double* __restrict__ scalars,
+                                        const unsigned long long* __restrict__ fail,
+                                        double* __restrict__ out) {
+  const bool failed = fail[0] != ~0ull || fail[1] != ~0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nch;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[1 + chunk_lo + i] = (failed && i == 0) ? __longlong_as_double(0x7ff8000000000000ll)
+                                               : partials[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (has_first) out[0] = scalars[1];
+    if (failed && nch == 0) out[0] = __longlong_as_double(0x7ff8000000000000ll);
+  }
+}
+
 __global__ void cov_eval_kernel(CovParams cp, const double* __restrict__ d, int64_t count,
                                 double* __restrict__ out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -100,6 +116,16 @@ cudaError_t launch_reduce(const Plan& p, bool want_total, cudaStream_t stream) {
                                                              p.chunk_lo, p.chunk_hi, p.d_partials);
   }
   if (want_total) total_kernel<<<1, 1, 0, stream>>>(p.d_partials, nch, p.d_scalars);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_partials(const Plan& p, double* d_out, cudaStream_t stream) {
+  int64_t nch = p.chunk_hi - p.chunk_lo;
+  unsigned blocks = (unsigned)((nch + 255) / 256);
+  if (blocks < 1) blocks = 1;
+  scatter_partials_kernel<<<blocks, 256, 0, stream>>>(p.d_partials, nch, p.chunk_lo,
+                                                       p.blk_lo == 0 ? 1 : 0, p.d_scalars,
+                                                       p.d_fail, d_out);
   return cudaGetLastError();
 }
 

@@ -205,6 +205,24 @@ class DevicePlan:
         N.check(rc)
         return parts[: self.nchunks], float(bf[0]), int(rc), int(fail[0])
 
+    def partials_device(self, spec: kernels.KernelSpec, out_ptr: int) -> None:
+        """Write block_first / this shard's chunk partials into a device vector
+        (see vgp_loglik_partials_device) for a cross-GPU all-reduce."""
+        p = spec.params
+        N.check(N.lib.vgp_loglik_partials_device(self.handle, N.FAMILY_CODES[spec.family],
+                                                 float(p.sigma_sq), float(p.beta), float(p.nu),
+                                                 ctypes.c_void_p(out_ptr)))
+
+    def set_timing(self, enable: bool) -> None:
+        N.check(N.lib.vgp_plan_set_timing(self.handle, 1 if enable else 0))
+
+    def kernel_time(self):
+        """(summed ms, launches) of the fused block kernel since the last call."""
+        ms = np.zeros(1)
+        cnt = np.zeros(1, dtype=np.int64)
+        N.check(N.lib.vgp_plan_kernel_time(self.handle, N.dptr(ms), N.iptr(cnt)))
+        return float(ms[0]), int(cnt[0])
+
     # -- launch-only interface for device-timed benchmarking
     def launch(self, spec: kernels.KernelSpec) -> None:
         p = spec.params
