@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -412,6 +413,7 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
   p->chunk_lo = rest_lo / kReduceChunk;
   p->chunk_hi = (p->rest_hi + kReduceChunk - 1) / kReduceChunk;
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* tv = std::getenv("VGP_TUNE")) p->tune = std::atoi(tv);
   p->events = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
   p->event_pool = new std::vector<cudaEvent_t>();
   const int64_t nrest = p->rest_hi - p->rest_lo;

@@ -77,56 +77,50 @@ __device__ __forceinline__ double cov_fast(double d, double inv_beta,
 template <int NT>
 struct Smem {
   static constexpr int kP = 8 * NT;
-  static constexpr int kTiles = NT * (NT + 1) / 2;
   static constexpr int kPanelLd = 10;  // panel row stride (doubles): conflict-free LDS.128 rows
-  // per warp: tile store (reused as the panel), (x, y) pairs, obs, 2 outputs
-  static constexpr int kWarpDoubles = kTiles * 64 + 2 * kP + kP + 2;
-  static constexpr int kMaxEntries = (kP - 2) * (kP - 1) / 2;  // m (m+1) / 2 with m <= P - 2
-  // [256 exp table][entry table (u32, padded to doubles)][warps]
-  static constexpr size_t entry_doubles() { return ((kMaxEntries + 3) / 4) * 2; }  // 16 B aligned
-  static constexpr size_t bytes() {
-    return sizeof(double) * (256 + entry_doubles() + (size_t)kWarps * kWarpDoubles);
-  }
+  // per warp: panel (kP rows), (x, y) pairs, obs, 2 outputs
+  static constexpr int kWarpDoubles = kP * kPanelLd + 2 * kP + kP + 2;
+  static constexpr size_t bytes() { return sizeof(double) * (256 + (size_t)kWarps * kWarpDoubles); }
 };
 
-template <int NT, int KIND>
-__global__ void __launch_bounds__(kWarps * 32)
-loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
+// minimum resident CTAs per SM: 3 x 4 warps for the 8x8-tile case caps the
+// register file at 168 per thread (the 36 accumulator tiles alone take 144).
+template <int NT>
+struct Occupancy {
+  static constexpr int kMinCtas = NT >= 8 ? 3 : (NT >= 6 ? 4 : 6);
+};
+
+// MC > 0 compiles the kernel for m == MC exactly: every panel extent, the
+// location of sigma_new / -mu and all padding tests fold away, leaving
+// branch-free straight-line code for the hot configurations (m = 30, 60).
+template <int NT, int KIND, int MC, int MINB = Occupancy<NT>::kMinCtas>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
+loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
               int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
               double* __restrict__ rest, double* __restrict__ mu_out,
               double* __restrict__ sig_out, unsigned long long* __restrict__ fail) {
   using S = Smem<NT>;
   constexpr int P = S::kP;
-  constexpr int NTILE = S::kTiles;
+  constexpr int NTILE = NT * (NT + 1) / 2;
   constexpr int LD = S::kPanelLd;
+  const int m = MC > 0 ? MC : m_rt;
   extern __shared__ __align__(16) double smem[];
   double* tab = smem;  // 256: sigma^2 * 2^(j/256)
-  uint32_t* ent = reinterpret_cast<uint32_t*>(smem + 256);  // packed (i, k, tile address)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2;  // fragment row
   const int q = lane & 3;   // fragment column pair
-  double* tiles = smem + 256 + S::entry_doubles() + (size_t)warp * S::kWarpDoubles;
-  double2* XY = reinterpret_cast<double2*>(tiles + NTILE * 64);
-  double* O = tiles + NTILE * 64 + 2 * P;
+  double* pan = smem + 256 + (size_t)warp * S::kWarpDoubles;
+  double2* XY = reinterpret_cast<double2*>(pan + P * LD);
+  double* O = pan + P * LD + 2 * P;
   double* out2 = O + P;
 
-  // per-CTA tables: exp table scaled by sigma^2 and the strictly-lower entry
-  // list of rows 1..m (row m = the target's cross-covariances v)
-  const int nent = m * (m + 1) / 2;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = s2 * kExp2Table[i];
-  for (int idx = threadIdx.x; idx < nent; idx += blockDim.x) {
-    int i = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)idx)) * 0.5f);
-    while (i * (i - 1) / 2 > idx) --i;
-    while ((i + 1) * i / 2 <= idx) ++i;
-    const int k = idx - i * (i - 1) / 2;
-    ent[idx] = (uint32_t)i | ((uint32_t)k << 8) | ((uint32_t)tile_addr(i, k) << 16);
-  }
   __syncthreads();
 
   const int64_t stride = (int64_t)gridDim.x * kWarps;
   for (int64_t e = e_lo + (int64_t)blockIdx.x * kWarps + warp; e < e_hi; e += stride) {
-    // ---------------- gather (index m = target) + zero the tile store ----------------
+    // ---------------- gather (index m = target) ----------------
     const int32_t* J = nbr + (e - 1 - rest_lo) * (int64_t)m;
     for (int a = lane; a < P; a += 32) {
       double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -135,120 +129,124 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
       XY[a] = make_double2(p.x, p.y);
       O[a] = p.z;
     }
-#pragma unroll
-    for (int T = 0; T < NTILE; ++T)
-      reinterpret_cast<double2*>(tiles + T * 64)[lane] = make_double2(0.0, 0.0);
     __syncwarp();
 
-    // ---------------- generate (entries spread evenly over lanes) ----------------
-#pragma unroll 2
-    for (int idx = lane; idx < nent; idx += 32) {
-      const uint32_t w = ent[idx];
-      const double2 a = XY[w & 0xff];
-      const double2 b = XY[(w >> 8) & 0xff];
-      const double dx = a.x - b.x;
-      const double dy = a.y - b.y;
-      const double d = sqrt_pos(fma(dx, dx, dy * dy));
-      tiles[w >> 16] = cov_fast<KIND>(d, inv_beta, tab);
-    }
-    for (int a = lane; a <= m; a += 32) tiles[tile_addr(a, a)] = s2;          // C(0) = sigma^2
-    for (int b = lane; b < m; b += 32) tiles[tile_addr(m + 1, b)] = O[b];     // yJ row
-    __syncwarp();
-
-    // ---------------- load the accumulator fragments ----------------
+    // ---------------- generate straight into accumulator fragments ----------------
+    // lane (r, q) owns entries (8I + r, 8J + 2q + h) of tile (I, J), I >= J.
+    // Rows below 8 (NT - 1) are always covariance rows (m >= 8 NT - 9), so
+    // only the diagonal tiles and the last tile row need entry tests.
     double t[NTILE][2];
 #pragma unroll
-    for (int T = 0; T < NTILE; ++T) {
-      const double2 v = reinterpret_cast<const double2*>(tiles + T * 64 + 8 * r)[q];
-      t[T][0] = v.x;
-      t[T][1] = v.y;
+    for (int I = 0; I < NT; ++I) {
+      const int a = 8 * I + r;
+      const double2 pa = XY[a];
+#pragma unroll
+      for (int Jt = 0; Jt <= I; ++Jt) {
+        const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * Jt + 2 * q);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int b = 8 * Jt + 2 * q + h;
+          const double dx = pa.x - (h ? pb.z : pb.x);
+          const double dy = pa.y - (h ? pb.w : pb.y);
+          // + 2^-1000: exact duplicates give d ~ 1e-150, C = sigma^2 to the last bit
+          const double d2 = fma(dx, dx, fma(dy, dy, 0x1p-1000));
+          double val = cov_fast<KIND>(sqrt_pos_nz(d2), inv_beta, tab);
+          if (I == NT - 1 || Jt == I) {
+            if (!(a <= m && b < a)) val = 0.0;
+            if (a == b && a <= m) val = s2;       // C(0) = sigma^2
+            if (a == m + 1 && b < m) val = O[b];  // yJ row
+          }
+          t[tidx(I, Jt)][h] = val;
+        }
+      }
     }
-    __syncwarp();
-    double* pan = tiles;  // tile store is free now: reuse as the panel buffer
 
-    // ---------------- blocked right-looking Cholesky ----------------
-    int failed = -1;
+    // ---------------- blocked right-looking Cholesky with look-ahead ----------------
+    // Panel c lives in registers in row-owner layout (lane l: panel rows l, l+32)
+    // and is factored column by column; the next pivot is formed by its owner
+    // from its own row, so one shuffle sits on the pivot-to-pivot chain.  After
+    // panel c, tile column c+1 is updated first and handed to the next panel;
+    // the rest of the trailing update is issued after, where it overlaps the
+    // next panel's dependent chain.  Failures are tracked without branching
+    // (fj: first non-positive pivot column) and acted on once per block.
+    constexpr int kMaxRows = 2;
+    int fj = -1;
+    double a[kMaxRows][8];
+    auto load_panel = [&](const int c) {
+      const int NR = P - 8 * c;
+#pragma unroll
+      for (int I = c; I < NT; ++I)
+        *reinterpret_cast<double2*>(pan + (8 * (I - c) + r) * LD + 2 * q) =
+            make_double2(t[tidx(I, c)][0], t[tidx(I, c)][1]);
+      __syncwarp();
+#pragma unroll
+      for (int rr = 0; rr < kMaxRows; ++rr) {
+        const int row = lane + 32 * rr;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          double2 v = make_double2(0.0, 0.0);
+          if (rr * 32 < NR && row < NR) v = *reinterpret_cast<const double2*>(pan + row * LD + 2 * x);
+          a[rr][2 * x] = v.x;
+          a[rr][2 * x + 1] = v.y;
+        }
+      }
+      __syncwarp();
+    };
+    load_panel(0);
 #pragma unroll
     for (int c = 0; c < NT; ++c) {
-      const int jmax = min(8, m - 8 * c);  // pivots in this tile column
-      if (jmax > 0 && failed < 0) {
-        constexpr int kMaxRows = 2;
-        const int R0 = 8 * c;       // first panel row
-        const int NR = P - R0;      // panel rows
-        const int ROWS = (NR + 31) / 32;
-        // registers -> row-major panel
-#pragma unroll
-        for (int I = c; I < NT; ++I)
-          *reinterpret_cast<double2*>(pan + (8 * (I - c) + r) * LD + 2 * q) =
-              make_double2(t[tidx(I, c)][0], t[tidx(I, c)][1]);
-        __syncwarp();
-        double a[kMaxRows][8];
-#pragma unroll
-        for (int rr = 0; rr < kMaxRows; ++rr) {
-          if (rr < ROWS) {
-            const int row = lane + 32 * rr;
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-              double2 v = make_double2(0.0, 0.0);
-              if (row < NR) v = *reinterpret_cast<const double2*>(pan + row * LD + 2 * x);
-              a[rr][2 * x] = v.x;
-              a[rr][2 * x + 1] = v.y;
-            }
-          }
-        }
-        // column-by-column factorization of the panel; lane l owns panel rows l, l + 32
+      const int R0 = 8 * c;
+      const int NR = P - R0;
+      const int jmax = min(8, m - R0);  // pivots in this tile column
+      if (jmax > 0) {
+        double piv = shfl(a[0][0], 0);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if (j < jmax && failed < 0) {
-            const double piv = shfl(a[0][j], j);
-            if (!(piv > 0.0)) {
-              failed = R0 + j;
-            } else {
-              const double inv = rsqrt_pos(piv);
-              const double ljj = piv * inv;
+          if (j < jmax) {
+            if (!(piv > 0.0) && fj < 0) fj = R0 + j;
+            const double inv = rsqrt_pos3(piv);
+            const double ljj = piv * inv;
+#pragma unroll
+            for (int rr = 0; rr < kMaxRows; ++rr)
+              if (rr * 32 < NR) a[rr][j] = (rr == 0 && lane == j) ? ljj : a[rr][j] * inv;
+            if (j + 1 < 8) {
+              const double nxt = fma(-a[0][j], a[0][j], a[0][j + 1]);  // lane j+1's pivot
+              piv = shfl(nxt, j + 1);
+            }
+#pragma unroll
+            for (int jp = j + 1; jp < 8; ++jp) {
+              const double lc = shfl(a[0][j], jp);  // L[R0 + jp][j]
 #pragma unroll
               for (int rr = 0; rr < kMaxRows; ++rr)
-                if (rr < ROWS) a[rr][j] = (rr == 0 && lane == j) ? ljj : a[rr][j] * inv;
+                if (rr * 32 < NR) a[rr][jp] = fma(-a[rr][j], lc, a[rr][jp]);
+            }
+          }
+        }
+        // sigma_new / -mu sit in this panel's first unfactored column
+        if (m - R0 < 8) {
+          const int cs = m - R0;
 #pragma unroll
-              for (int jp = j + 1; jp < 8; ++jp) {
-                const double lc = shfl(a[0][j], jp);  // L[R0 + jp][j]
+          for (int rr = 0; rr < kMaxRows; ++rr) {
+            if (rr * 32 < NR) {
+              const int row = lane + 32 * rr;
 #pragma unroll
-                for (int rr = 0; rr < kMaxRows; ++rr)
-                  if (rr < ROWS) a[rr][jp] = fma(-a[rr][j], lc, a[rr][jp]);
+              for (int x = 0; x < 8; ++x) {
+                if (x == cs && row == m - R0) out2[0] = a[rr][x];
+                if (x == cs && row == m + 1 - R0) out2[1] = a[rr][x];
               }
             }
           }
         }
-        if (failed < 0) {
-          // sigma_new / -mu sit in this panel when m is not a multiple of 8
-          if (jmax < 8 || (m & 7) != 0) {
-            const int cs = m - R0;  // panel column of index m (only meaningful if < 8)
-            if (cs < 8) {
-#pragma unroll
-              for (int rr = 0; rr < kMaxRows; ++rr) {
-                if (rr < ROWS) {
-                  const int row = lane + 32 * rr;
-#pragma unroll
-                  for (int x = 0; x < 8; ++x) {
-                    if (x == cs && row == m - R0) out2[0] = a[rr][x];
-                    if (x == cs && row == m + 1 - R0) out2[1] = a[rr][x];
-                  }
-                }
-              }
-            }
-          }
-          // panel -> shared memory, then A-fragments frag_kk(T) = L[8I + r][4 kk + q]
-          __syncwarp();
+        if (c + 1 < NT) {
+          // L panel -> shared memory -> A-fragments frag_kk(T) = L[8I + r][4 kk + q]
 #pragma unroll
           for (int rr = 0; rr < kMaxRows; ++rr) {
-            if (rr < ROWS) {
-              const int row = lane + 32 * rr;
-              if (row < NR) {
+            const int row = lane + 32 * rr;
+            if (rr * 32 < NR && row < NR) {
 #pragma unroll
-                for (int x = 0; x < 4; ++x)
-                  *reinterpret_cast<double2*>(pan + row * LD + 2 * x) =
-                      make_double2(a[rr][2 * x], a[rr][2 * x + 1]);
-              }
+              for (int x = 0; x < 4; ++x)
+                *reinterpret_cast<double2*>(pan + row * LD + 2 * x) =
+                    make_double2(a[rr][2 * x], a[rr][2 * x + 1]);
             }
           }
           __syncwarp();
@@ -259,13 +257,20 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
             for (int kk = 0; kk < 2; ++kk) fa[I][kk] = pan[(8 * (I - c) + r) * LD + 4 * kk + q];
           }
           __syncwarp();
-          // trailing update A_IJ -= L_Ic L_Jc^T, c < J <= I
+          // look-ahead: tile column c+1 first, then hand it to the next panel
 #pragma unroll
           for (int I = c + 1; I < NT; ++I) {
+            mma884(t[tidx(I, c + 1)][0], t[tidx(I, c + 1)][1], neg(fa[I][0]), fa[c + 1][0]);
+            mma884(t[tidx(I, c + 1)][0], t[tidx(I, c + 1)][1], neg(fa[I][1]), fa[c + 1][1]);
+          }
+          if (m - 8 * (c + 1) > 0) load_panel(c + 1);
+          // remaining trailing update A_IJ -= L_Ic L_Jc^T, c + 1 < J <= I
+#pragma unroll
+          for (int I = c + 2; I < NT; ++I) {
             const double n0 = neg(fa[I][0]);
             const double n1 = neg(fa[I][1]);
 #pragma unroll
-            for (int Jt = c + 1; Jt <= I; ++Jt) {
+            for (int Jt = c + 2; Jt <= I; ++Jt) {
               mma884(t[tidx(I, Jt)][0], t[tidx(I, Jt)][1], n0, fa[Jt][0]);
               mma884(t[tidx(I, Jt)][0], t[tidx(I, Jt)][1], n1, fa[Jt][1]);
             }
@@ -276,8 +281,8 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
 
     // ---------------- per-block log-density ----------------
     const int64_t kk = e - 1 - rest_lo;
-    if (failed >= 0) {
-      if (lane == 0) atomicMin(&fail[0], npd_key(e, failed, m));
+    if (fj >= 0) {
+      if (lane == 0) atomicMin(&fail[0], npd_key(e, fj, m));
     } else {
       if ((m & 7) == 0) {
         // m = 8 (NT - 1): sigma_new = tile (NT-1, NT-1)[0][0], -mu = [1][0]
@@ -303,14 +308,14 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
   }
 }
 
-template <int NT, int KIND>
+template <int NT, int KIND, int MC, int MINB = Occupancy<NT>::kMinCtas>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream) {
   const size_t sm = Smem<NT>::bytes();
   static bool configured[64] = {};  // per device ordinal
   const int dev = p.device & 63;
   if (!configured[dev]) {
-    cudaError_t err = cudaFuncSetAttribute(loglik_kernel<NT, KIND>,
+    cudaError_t err = cudaFuncSetAttribute(loglik_kernel<NT, KIND, MC, MINB>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
     configured[dev] = true;
@@ -319,7 +324,7 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   const int64_t want = (count + kWarps - 1) / kWarps;
   const int64_t cap = (int64_t)p.num_sms * 16;
   const int grid = (int)(want < cap ? want : cap);
-  loglik_kernel<NT, KIND><<<grid, kWarps * 32, sm, stream>>>(
+  loglik_kernel<NT, KIND, MC, MINB><<<grid, kWarps * 32, sm, stream>>>(
       p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2, cp.inv_beta, p.d_rest, p.d_mu,
       p.d_sig, p.d_fail);
   return cudaGetLastError();
@@ -328,15 +333,20 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
 template <int KIND>
 cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                         cudaStream_t stream) {
+  if (p.m == 60) {
+    if (p.tune == 2) return launch<8, KIND, 60, 2>(p, cp, e_lo, e_hi, stream);
+    return launch<8, KIND, 60>(p, cp, e_lo, e_hi, stream);
+  }
+  if (p.m == 30) return launch<4, KIND, 30>(p, cp, e_lo, e_hi, stream);
   switch ((p.m + 2 + 7) / 8) {
-    case 1: return launch<1, KIND>(p, cp, e_lo, e_hi, stream);
-    case 2: return launch<2, KIND>(p, cp, e_lo, e_hi, stream);
-    case 3: return launch<3, KIND>(p, cp, e_lo, e_hi, stream);
-    case 4: return launch<4, KIND>(p, cp, e_lo, e_hi, stream);
-    case 5: return launch<5, KIND>(p, cp, e_lo, e_hi, stream);
-    case 6: return launch<6, KIND>(p, cp, e_lo, e_hi, stream);
-    case 7: return launch<7, KIND>(p, cp, e_lo, e_hi, stream);
-    case 8: return launch<8, KIND>(p, cp, e_lo, e_hi, stream);
+    case 1: return launch<1, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 2: return launch<2, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 3: return launch<3, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 4: return launch<4, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 5: return launch<5, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 6: return launch<6, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 7: return launch<7, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 8: return launch<8, KIND, 0>(p, cp, e_lo, e_hi, stream);
     default: return cudaErrorNotSupported;
   }
 }

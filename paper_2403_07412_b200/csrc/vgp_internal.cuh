@@ -85,6 +85,7 @@ struct Plan {
   int64_t chunk_lo = 0, chunk_hi = 0;  // global 4096-chunk ids covered (rest range aligned)
   int kernel_variant = -1;      // last kernel used (for introspection)
   int force_variant = -1;       // -1 auto
+  int tune = 0;                 // experiment selector (env VGP_TUNE at plan creation)
   bool timing = false;          // record events around the fused kernel
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* events = nullptr;  // pending pairs
   std::vector<cudaEvent_t>* event_pool = nullptr;
