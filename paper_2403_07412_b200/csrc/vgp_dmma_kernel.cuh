@@ -83,11 +83,12 @@ struct Smem {
   static constexpr size_t bytes() { return sizeof(double) * (256 + (size_t)kWarps * kWarpDoubles); }
 };
 
-// minimum resident CTAs per SM: 3 x 4 warps for the 8x8-tile case caps the
-// register file at 168 per thread (the 36 accumulator tiles alone take 144).
+// minimum resident CTAs per SM (register cap 65536 / (128 * kMinCtas)): the
+// 36 accumulator tiles of NT = 8 alone take 144 registers, and a 168 cap
+// (3 CTAs) spilled and measured slower than 2 CTAs without spills.
 template <int NT>
 struct Occupancy {
-  static constexpr int kMinCtas = NT >= 8 ? 3 : (NT >= 6 ? 4 : 6);
+  static constexpr int kMinCtas = NT >= 7 ? 2 : (NT >= 5 ? 3 : (NT >= 3 ? 4 : 6));
 };
 
 // MC > 0 compiles the kernel for m == MC exactly: every panel extent, the
@@ -119,15 +120,34 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
   __syncthreads();
 
   const int64_t stride = (int64_t)gridDim.x * kWarps;
-  for (int64_t e = e_lo + (int64_t)blockIdx.x * kWarps + warp; e < e_hi; e += stride) {
-    // ---------------- gather (index m = target) ----------------
-    const int32_t* J = nbr + (e - 1 - rest_lo) * (int64_t)m;
-    for (int a = lane; a < P; a += 32) {
-      double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (a < m) p = pts[J[a]];
-      else if (a == m) p = pts[m + e - 1];
-      XY[a] = make_double2(p.x, p.y);
-      O[a] = p.z;
+  // Software-pipelined gather: block e+stride's neighbour indices are read
+  // during block e's first panel and its points during the second-to-last
+  // panel, so the dependent L2 round trips overlap the factorization.
+  // Lane owns conditioning-set slots lane and lane + 32 (index m = target).
+  auto slot_index = [&](int64_t eb, int a) -> int {
+    if (a < m) return nbr[(eb - 1 - rest_lo) * (int64_t)m + a];
+    return a == m ? (int)(m + eb - 1) : -1;
+  };
+  auto slot_point = [&](int idx) -> double4 {
+    return idx >= 0 ? pts[idx] : make_double4(0.0, 0.0, 0.0, 0.0);
+  };
+  int64_t e = e_lo + (int64_t)blockIdx.x * kWarps + warp;
+  int ni0 = -1, ni1 = -1;
+  double4 pf0 = make_double4(0.0, 0.0, 0.0, 0.0), pf1 = pf0;
+  if (e < e_hi) {
+    pf0 = slot_point(slot_index(e, lane));
+    if (P > 32) pf1 = slot_point(slot_index(e, lane + 32));
+  }
+  for (; e < e_hi; e += stride) {
+    const int64_t en = e + stride;
+    // ---------------- gather (from the prefetch registers) ----------------
+    if (lane < P) {
+      XY[lane] = make_double2(pf0.x, pf0.y);
+      O[lane] = pf0.z;
+    }
+    if (P > 32 && lane + 32 < P) {
+      XY[lane + 32] = make_double2(pf1.x, pf1.y);
+      O[lane + 32] = pf1.z;
     }
     __syncwarp();
 
@@ -198,6 +218,14 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
       const int R0 = 8 * c;
       const int NR = P - R0;
       const int jmax = min(8, m - R0);  // pivots in this tile column
+      if (c == 0 && en < e_hi) {
+        ni0 = slot_index(en, lane);
+        if (P > 32) ni1 = slot_index(en, lane + 32);
+      }
+      if (c == (NT >= 2 ? NT - 2 : 0) && en < e_hi) {
+        pf0 = slot_point(ni0);
+        if (P > 32) pf1 = slot_point(ni1);
+      }
       if (jmax > 0) {
         double piv = shfl(a[0][0], 0);
 #pragma unroll
@@ -205,10 +233,9 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
           if (j < jmax) {
             if (!(piv > 0.0) && fj < 0) fj = R0 + j;
             const double inv = rsqrt_pos3(piv);
-            const double ljj = piv * inv;
 #pragma unroll
             for (int rr = 0; rr < kMaxRows; ++rr)
-              if (rr * 32 < NR) a[rr][j] = (rr == 0 && lane == j) ? ljj : a[rr][j] * inv;
+              if (rr * 32 < NR) a[rr][j] *= inv;  // the pivot row's own entry becomes piv * inv = L_jj
             if (j + 1 < 8) {
               const double nxt = fma(-a[0][j], a[0][j], a[0][j + 1]);  // lane j+1's pivot
               piv = shfl(nxt, j + 1);
@@ -334,7 +361,7 @@ template <int KIND>
 cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                         cudaStream_t stream) {
   if (p.m == 60) {
-    if (p.tune == 2) return launch<8, KIND, 60, 2>(p, cp, e_lo, e_hi, stream);
+    if (p.tune == 3) return launch<8, KIND, 60, 3>(p, cp, e_lo, e_hi, stream);
     return launch<8, KIND, 60>(p, cp, e_lo, e_hi, stream);
   }
   if (p.m == 30) return launch<4, KIND, 30>(p, cp, e_lo, e_hi, stream);

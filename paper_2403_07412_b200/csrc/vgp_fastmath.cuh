@@ -64,7 +64,7 @@ __device__ __forceinline__ double rsqrt_pos3(double x) {
 }
 
 // tab[j] = scale * 2^(j/256) (shared memory).  Returns scale * exp(-u) for
-// u >= 0, and 0 once the result would leave the normal range (u > 690).
+// u >= 0 (results below ~1e-290 are not guaranteed exact; see below).
 __device__ __forceinline__ double exp_neg_tab(double u, const double* __restrict__ tab) {
   const double shift = 0x1.8p52;
   const double t = fma(-u, k256OverLn2, shift);  // round(-u * 256 / ln 2) in the low word
@@ -77,9 +77,11 @@ __device__ __forceinline__ double exp_neg_tab(double u, const double* __restrict
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = tab[ki & 255] * p;
-  const int e = ki >> 8;  // arithmetic shift: floor(k / 256)
-  const double out = __hiloint2double(__double2hiint(v) + (e << 20), __double2loint(v));
-  return (ki < -254000) ? 0.0 : out;  // integer test: u > ~688
+  // 2^e by adding e to the exponent field (one IMAD); e is clamped at -1000
+  // so deep underflow returns ~1e-301 * v instead of wrapping (such entries
+  // are below any Cholesky rounding and the reference's exp underflows them).
+  const int e = max(ki >> 8, -1000);
+  return __hiloint2double(__double2hiint(v) + e * 0x100000, __double2loint(v));
 }
 
 }  // namespace vgp
