@@ -59,6 +59,16 @@ def ordered_total(vec: np.ndarray) -> float:
     return float(vec[0]) + s
 
 
+def combine_partials(send, buf, dist, group=None) -> np.ndarray:
+    """The one collective of an evaluation: every rank's `send` holds its own
+    slots (block_first at 0 for rank 0, its chunk partials at 1 + c) and zeros
+    elsewhere; SUM-all-reduce into `buf` and return it on the host.  Device
+    agnostic (NCCL on CUDA tensors, gloo on CPU tensors in the tests)."""
+    buf.copy_(send)
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf.cpu().numpy()
+
+
 class ShardedVecchia:
     """The MLE objective on this rank's shard: `total(spec)` is collective."""
 
@@ -88,9 +98,7 @@ class ShardedVecchia:
     def reduce_vector(self, spec) -> np.ndarray:
         if self.dplan is not None:
             self.dplan.partials_device(spec, self.send.data_ptr())
-        self.buf.copy_(self.send)
-        self.dist.all_reduce(self.buf, op=self.dist.ReduceOp.SUM, group=self.group)
-        return self.buf.cpu().numpy()
+        return combine_partials(self.send, self.buf, self.dist, self.group)
 
     def total(self, spec) -> float:
         vec = self.reduce_vector(spec)

@@ -295,6 +295,11 @@ def vecchia_loglik(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.Kernel
     return dp.loglik(spec)
 
 
+# The package's own implementation, so callers can tell whether the module
+# attribute (the reference's plugin seam, vg/fit.py:165) has been replaced.
+NATIVE_VECCHIA_LOGLIK = vecchia_loglik
+
+
 def _ordered_sum(values: np.ndarray) -> float:
     """4096-chunk pairwise partials combined in index order (vg/vecchia.py:169-177)."""
     partials = [float(values[lo:lo + _REDUCE_CHUNK].sum())
