@@ -293,7 +293,7 @@ def run_ours_single(args):
         "gpu_launches": KERNELS_PER_EVAL * args.steps,
         "clocks": clk.summary(),
         "knn_s": knn_s, "total": total,
-        "kernel_variant": "warp-dmma" if dp.kernel_variant == 1 else "generic",
+        "kernel_variant": {0: "generic", 1: "warp-dmma", 2: "warp-dmma+dcache"}.get(dp.kernel_variant, "?"),
     }
     if not args.no_cpu_baseline:
         ordered = data.permute(plan.permutation)

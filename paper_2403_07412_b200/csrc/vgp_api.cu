@@ -146,6 +146,9 @@ void free_plan(Plan* p) {
   cudaFree(p->d_scalars);
   cudaFree(p->d_fail);
   cudaFree(p->d_work);
+  cudaFree(p->d_dcache);
+  cudaFree(p->d_prev_locs);
+  cudaFree(p->d_flag);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->h_small) cudaFreeHost(p->h_small);
   if (p->events) {
@@ -196,9 +199,15 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
       if (rc) return rc;
       VGP_CUDA_TRY(cudaEventRecord(ev0, s));
     }
+    if (p->force_variant == 2 && !use_dmma)
+      return fail(VGP_E_UNSUPPORTED, "warp-DMMA variant does not cover this m / kernel");
     if (use_dmma) {
-      VGP_CUDA_TRY(launch_loglik_dmma(*p, cp, e_lo, e_hi, s));
-      p->kernel_variant = 1;
+      const bool keep = p->dcache_valid;
+      if (p->force_variant == 2) p->dcache_valid = false;
+      cudaError_t err = launch_loglik_dmma(*p, cp, e_lo, e_hi, s);
+      p->dcache_valid = keep;
+      VGP_CUDA_TRY(err);
+      p->kernel_variant = (p->d_dcache && p->dcache_valid && p->force_variant != 2) ? 2 : 1;
     } else {
       VGP_CUDA_TRY(launch_loglik_generic(*p, cp, e_lo, e_hi, s));
       p->kernel_variant = 0;
@@ -445,6 +454,31 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
       rc = dalloc(&p->d_work, p->work_doubles);
     }
   }
+  if (!rc && nrest > 0 && dmma_supported(m, kMatern15) && metric == VGP_METRIC_EUCLIDEAN) {
+    // distance cache: on unless VGP_DCACHE=0, and only when it fits in half
+    // of the free device memory
+    const char* env = std::getenv("VGP_DCACHE");
+    const bool want = !(env && env[0] == '0');
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    const int64_t stride = dcache_stride(m);
+    const size_t bytes = sizeof(double) * (size_t)stride * (size_t)nrest;
+    if (want && bytes < freeb / 2) {
+      if (cudaMalloc((void**)&p->d_dcache, bytes) == cudaSuccess &&
+          cudaMalloc((void**)&p->d_prev_locs, sizeof(double) * 2 * (size_t)n) == cudaSuccess &&
+          cudaMalloc((void**)&p->d_flag, sizeof(int)) == cudaSuccess) {
+        p->dcache_stride = stride;
+      } else {
+        cudaFree(p->d_dcache);
+        cudaFree(p->d_prev_locs);
+        cudaFree(p->d_flag);
+        p->d_dcache = nullptr;
+        p->d_prev_locs = nullptr;
+        p->d_flag = nullptr;
+        cudaGetLastError();
+      }
+    }
+  }
   if (!rc && cudaMallocHost((void**)&p->h_small, 64) != cudaSuccess)
     rc = fail(VGP_E_NOMEM, "cudaMallocHost small");
   if (rc) {
@@ -491,6 +525,24 @@ int vgp_plan_set_data(vgp_plan* plan, const double* locations, const double* obs
   VGP_CUDA_TRY(cudaMemcpyAsync(p->d_raw + 2 * n, observations, sizeof(double) * n,
                                cudaMemcpyHostToDevice, p->stream));
   VGP_CUDA_TRY(launch_permute(p->d_raw, p->d_order, n, p->d_pts, p->stream));
+  if (p->d_dcache) {
+    // rebuild the distance cache only when the locations changed
+    bool rebuild = !p->dcache_valid;
+    if (!rebuild) {
+      int* hflag = (int*)(p->h_small + 6);
+      VGP_CUDA_TRY(cudaMemsetAsync(p->d_flag, 0, sizeof(int), p->stream));
+      VGP_CUDA_TRY(launch_diff(p->d_raw, p->d_prev_locs, 2 * n, p->d_flag, p->stream));
+      VGP_CUDA_TRY(cudaMemcpyAsync(hflag, p->d_flag, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+      VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+      rebuild = *hflag != 0;
+    }
+    if (rebuild) {
+      VGP_CUDA_TRY(cudaMemcpyAsync(p->d_prev_locs, p->d_raw, sizeof(double) * 2 * n,
+                                   cudaMemcpyDeviceToDevice, p->stream));
+      VGP_CUDA_TRY(launch_build_dcache(*p, p->stream));
+      p->dcache_valid = true;
+    }
+  }
   VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
   p->has_data = true;
   return VGP_OK;
@@ -516,6 +568,7 @@ int vgp_plan_info(const vgp_plan* plan, int64_t* info) {
   info[5] = p.chunk_hi - p.chunk_lo;
   info[6] = p.kernel_variant;
   info[7] = p.device;
+  info[8] = (p.d_dcache && p.dcache_valid) ? 1 : 0;
   return VGP_OK;
 }
 
@@ -563,7 +616,8 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 1) return fail(VGP_E_INVALID, "bad variant");
+  if (!plan || variant < -1 || variant > 2) return fail(VGP_E_INVALID, "bad variant");
+  // 2 = warp-DMMA without the distance cache (testing aid)
   plan->p.force_variant = variant;
   return VGP_OK;
 }

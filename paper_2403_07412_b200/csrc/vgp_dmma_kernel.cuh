@@ -78,10 +78,46 @@ template <int NT>
 struct Smem {
   static constexpr int kP = 8 * NT;
   static constexpr int kPanelLd = 10;  // panel row stride (doubles): conflict-free LDS.128 rows
-  // per warp: panel (kP rows), (x, y) pairs, obs, 2 outputs
-  static constexpr int kWarpDoubles = kP * kPanelLd + 2 * kP + kP + 2;
-  static constexpr size_t bytes() { return sizeof(double) * (256 + (size_t)kWarps * kWarpDoubles); }
+  // per warp: panel (kP rows), (x, y) pairs, obs, 2 outputs, mbarrier
+  static constexpr int kWarpDoubles = kP * kPanelLd + 2 * kP + kP + 2 + 2;
+  // distance-cache buffer per warp (doubles), 16-byte aligned
+  static constexpr int cache_doubles(int m) { return ((m * (m + 1) / 2) + 1) & ~1; }
+  static size_t bytes(bool cache, int m) {
+    return sizeof(double) *
+           (256 + (size_t)kWarps * (kWarpDoubles + (cache ? cache_doubles(m) : 0)));
+  }
 };
+
+// ---- TMA bulk copy (cp.async.bulk, SASS UBLKCP) + mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 
 // minimum resident CTAs per SM (register cap 65536 / (128 * kMinCtas)): the
 // 36 accumulator tiles of NT = 8 alone take 144 registers, and a 168 cap
@@ -94,12 +130,18 @@ struct Occupancy {
 // MC > 0 compiles the kernel for m == MC exactly: every panel extent, the
 // location of sigma_new / -mu and all padding tests fold away, leaving
 // branch-free straight-line code for the hot configurations (m = 30, 60).
-template <int NT, int KIND, int MC, int MINB = Occupancy<NT>::kMinCtas>
+// CACHE: the plan holds every block's distances (compact strictly-lower order,
+// rows 1..m, built once per dataset by build_dcache_kernel); each warp streams
+// the next block's row of the cache into shared memory with a 1D TMA bulk copy
+// (cp.async.bulk + mbarrier) while it factors the current one, and the
+// generation skips the coordinate gather, the distance and the square root.
+template <int NT, int KIND, int MC, int MINB = Occupancy<NT>::kMinCtas, bool CACHE = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
               int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
               double* __restrict__ rest, double* __restrict__ mu_out,
-              double* __restrict__ sig_out, unsigned long long* __restrict__ fail) {
+              double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
+              const double* __restrict__ dcache, int64_t cstride) {
   using S = Smem<NT>;
   constexpr int P = S::kP;
   constexpr int NTILE = NT * (NT + 1) / 2;
@@ -115,9 +157,14 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
   double2* XY = reinterpret_cast<double2*>(pan + P * LD);
   double* O = pan + P * LD + 2 * P;
   double* out2 = O + P;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out2 + 2);
+  double* dbuf = smem + 256 + (size_t)kWarps * S::kWarpDoubles + (size_t)warp * cstride;
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = s2 * kExp2Table[i];
+  if (CACHE && lane == 0) mbar_init(bar);
   __syncthreads();
+  const uint32_t cbytes = (uint32_t)(cstride * sizeof(double));
+  uint32_t cphase = 0;
 
   const int64_t stride = (int64_t)gridDim.x * kWarps;
   // Software-pipelined gather: block e+stride's neighbour indices are read
@@ -135,6 +182,7 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
   int ni0 = -1, ni1 = -1;
   double4 pf0 = make_double4(0.0, 0.0, 0.0, 0.0), pf1 = pf0;
   if (e < e_hi) {
+    if (CACHE && lane == 0) bulk_load(dbuf, dcache + (e - 1 - rest_lo) * cstride, cbytes, bar);
     pf0 = slot_point(slot_index(e, lane));
     if (P > 32) pf1 = slot_point(slot_index(e, lane + 32));
   }
@@ -156,6 +204,33 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
     // Rows below 8 (NT - 1) are always covariance rows (m >= 8 NT - 9), so
     // only the diagonal tiles and the last tile row need entry tests.
     double t[NTILE][2];
+    if (CACHE) {
+      mbar_wait(bar, cphase);
+      cphase ^= 1;
+#pragma unroll
+      for (int I = 0; I < NT; ++I) {
+        const int a = 8 * I + r;
+        const int rowbase = a * (a - 1) / 2;  // compact index of (a, 0)
+#pragma unroll
+        for (int Jt = 0; Jt <= I; ++Jt) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int b = 8 * Jt + 2 * q + h;
+            const bool lower = (I < NT - 1 && Jt < I) || (b < a && a <= m);
+            double val = 0.0;
+            if (lower) val = cov_fast<KIND>(dbuf[rowbase + b], inv_beta, tab);
+            if (I == NT - 1 || Jt == I) {
+              if (a == b && a <= m) val = s2;       // C(0) = sigma^2
+              if (a == m + 1 && b < m) val = O[b];  // yJ row
+            }
+            t[tidx(I, Jt)][h] = val;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && en < e_hi)
+        bulk_load(dbuf, dcache + (en - 1 - rest_lo) * cstride, cbytes, bar);
+    } else {
 #pragma unroll
     for (int I = 0; I < NT; ++I) {
       const int a = 8 * I + r;
@@ -179,6 +254,7 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
           t[tidx(I, Jt)][h] = val;
         }
       }
+    }
     }
 
     // ---------------- blocked right-looking Cholesky with look-ahead ----------------
@@ -335,45 +411,50 @@ loglik_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, 
   }
 }
 
-template <int NT, int KIND, int MC, int MINB = Occupancy<NT>::kMinCtas>
+template <int NT, int KIND, int MC, int MINB = Occupancy<NT>::kMinCtas, bool CACHE = false>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream) {
-  const size_t sm = Smem<NT>::bytes();
-  static bool configured[64] = {};  // per device ordinal
+  const size_t sm = Smem<NT>::bytes(CACHE, p.m);
+  static size_t configured[64] = {};  // per device ordinal: smem size set
   const int dev = p.device & 63;
-  if (!configured[dev]) {
-    cudaError_t err = cudaFuncSetAttribute(loglik_kernel<NT, KIND, MC, MINB>,
+  if (configured[dev] < sm) {
+    cudaError_t err = cudaFuncSetAttribute(loglik_kernel<NT, KIND, MC, MINB, CACHE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
-    configured[dev] = true;
+    configured[dev] = sm;
   }
   const int64_t count = e_hi - e_lo;
   const int64_t want = (count + kWarps - 1) / kWarps;
   const int64_t cap = (int64_t)p.num_sms * 16;
   const int grid = (int)(want < cap ? want : cap);
-  loglik_kernel<NT, KIND, MC, MINB><<<grid, kWarps * 32, sm, stream>>>(
+  loglik_kernel<NT, KIND, MC, MINB, CACHE><<<grid, kWarps * 32, sm, stream>>>(
       p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2, cp.inv_beta, p.d_rest, p.d_mu,
-      p.d_sig, p.d_fail);
+      p.d_sig, p.d_fail, p.d_dcache, p.dcache_stride);
   return cudaGetLastError();
+}
+
+template <int NT, int KIND, int MC>
+cudaError_t launch_c(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                     cudaStream_t stream) {
+  if (p.d_dcache && p.dcache_valid)
+    return launch<NT, KIND, MC, Occupancy<NT>::kMinCtas, true>(p, cp, e_lo, e_hi, stream);
+  return launch<NT, KIND, MC, Occupancy<NT>::kMinCtas, false>(p, cp, e_lo, e_hi, stream);
 }
 
 template <int KIND>
 cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                         cudaStream_t stream) {
-  if (p.m == 60) {
-    if (p.tune == 3) return launch<8, KIND, 60, 3>(p, cp, e_lo, e_hi, stream);
-    return launch<8, KIND, 60>(p, cp, e_lo, e_hi, stream);
-  }
-  if (p.m == 30) return launch<4, KIND, 30>(p, cp, e_lo, e_hi, stream);
+  if (p.m == 60) return launch_c<8, KIND, 60>(p, cp, e_lo, e_hi, stream);
+  if (p.m == 30) return launch_c<4, KIND, 30>(p, cp, e_lo, e_hi, stream);
   switch ((p.m + 2 + 7) / 8) {
-    case 1: return launch<1, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 2: return launch<2, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 3: return launch<3, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 4: return launch<4, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 5: return launch<5, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 6: return launch<6, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 7: return launch<7, KIND, 0>(p, cp, e_lo, e_hi, stream);
-    case 8: return launch<8, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 1: return launch_c<1, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 2: return launch_c<2, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 3: return launch_c<3, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 4: return launch_c<4, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 5: return launch_c<5, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 6: return launch_c<6, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 7: return launch_c<7, KIND, 0>(p, cp, e_lo, e_hi, stream);
+    case 8: return launch_c<8, KIND, 0>(p, cp, e_lo, e_hi, stream);
     default: return cudaErrorNotSupported;
   }
 }

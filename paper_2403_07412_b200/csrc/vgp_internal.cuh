@@ -86,6 +86,11 @@ struct Plan {
   int kernel_variant = -1;      // last kernel used (for introspection)
   int force_variant = -1;       // -1 auto
   int tune = 0;                 // experiment selector (env VGP_TUNE at plan creation)
+  double* d_dcache = nullptr;   // per-block distance cache (compact lower rows 1..m)
+  int64_t dcache_stride = 0;    // doubles per block (16-byte multiple)
+  bool dcache_valid = false;
+  double* d_prev_locs = nullptr;  // locations the cache was built from (n x 2)
+  int* d_flag = nullptr;
   bool timing = false;          // record events around the fused kernel
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* events = nullptr;  // pending pairs
   std::vector<cudaEvent_t>* event_pool = nullptr;
@@ -115,6 +120,12 @@ bool dmma_supported(int m, int kind);
 // Scatter the shard's chunk partials (and block_first) into a global device
 // vector for the cross-GPU all-reduce; NaN-poison on failure.
 cudaError_t launch_scatter_partials(const Plan& p, double* d_out, cudaStream_t stream);
+
+// Distance cache (vgp_dcache.cu).
+int64_t dcache_stride(int m);
+cudaError_t launch_build_dcache(const Plan& p, cudaStream_t stream);
+cudaError_t launch_diff(const double* a, const double* b, int64_t n, int* flag,
+                        cudaStream_t stream);
 
 // numpy-pairwise 4096-chunk partials of d_rest and the ordered total.
 cudaError_t launch_reduce(const Plan& p, bool want_total, cudaStream_t stream);

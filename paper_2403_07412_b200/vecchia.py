@@ -144,7 +144,7 @@ class DevicePlan:
         return self._h
 
     def info(self) -> np.ndarray:
-        out = np.zeros(8, dtype=np.int64)
+        out = np.zeros(9, dtype=np.int64)
         N.check(N.lib.vgp_plan_info(self._h, N.iptr(out)))
         return out
 
@@ -153,7 +153,8 @@ class DevicePlan:
         return int(self.info()[6])
 
     def set_variant(self, variant: int) -> None:
-        """-1 auto, 0 generic kernel, 1 warp-DMMA kernel (testing aid)."""
+        """-1 auto, 0 generic, 1 warp-DMMA (+ distance cache if built), 2 warp-DMMA
+        without the cache (testing aid)."""
         N.check(N.lib.vgp_plan_set_variant(self.handle, int(variant)))
 
     def set_data(self, dataset: geo.Dataset) -> None:

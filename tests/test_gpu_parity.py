@@ -264,3 +264,35 @@ def test_c1_mle_matches_reference(vg):
     assert rel(fr.theta_hat.beta, float(th[1])) <= 1e-4
     assert fr.theta_hat.nu == 0.5
     assert rel(fr.loglik, float(z["mle_loglik"])) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["ll_n3000_m60_nu15", "ll_n2000_m30_nu15", "ll_n2000_m40_nu05_s2",
+                                  "ll_n1000_m20_nu25", "ll_n300_m10_nu05"])
+def test_distance_cache_is_bit_identical(vg, name):
+    """The plan-time distance cache stores exactly the distances the fused
+    kernel computes on the fly: cached and uncached evaluations agree bit
+    for bit."""
+    z = load(name)
+    data, plan, spec = _plan_from_golden(vg, z)
+    dp = plan.device_plan()
+    dp.set_variant(-1)
+    a = vg.vecchia_loglik(data, plan, spec)
+    cached = dp.info()[8] == 1
+    dp.set_variant(2)
+    b = vg.vecchia_loglik(data, plan, spec)
+    dp.set_variant(-1)
+    assert cached
+    assert a.total == b.total
+    np.testing.assert_array_equal(a.block_rest, b.block_rest)
+
+
+def test_distance_cache_rebuilt_when_locations_change(vg, oracle):
+    z = load("ll_n3000_m60_nu15")
+    data, plan, spec = _plan_from_golden(vg, z)
+    vg.vecchia_loglik(data, plan, spec)
+    moved = vg.Dataset(z["locs"] * 1.01, z["obs"])
+    got = vg.vecchia_loglik(moved, plan, spec).total
+    ordered = moved.permute(plan.permutation)
+    ref = oracle.loglik(ordered.locations, ordered.observations, int(z["m"]), z["table"], "matern",
+                        *[float(v) for v in z["theta"]])
+    assert rel(got, ref.total) <= TOL_TOTAL
