@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=-1,
+                    help="kernel variant (-1 auto, 0 generic, 1 all-register, 2 grouped, 3 warp-specialised, 4 warp-specialised+dcache)")
     return ap.parse_args()
 
 
@@ -232,6 +234,7 @@ def run_ours_single(args):
     spec = vg.KernelSpec("matern", vg.KernelParams(1.0, args.beta, args.nu))
     dp = plan.device_plan(dev)
     dp.set_data(data)
+    dp.set_variant(args.variant)
     stream = torch.cuda.ExternalStream(dp.stream)
 
     for _ in range(args.warmup):
@@ -293,7 +296,7 @@ def run_ours_single(args):
         "gpu_launches": KERNELS_PER_EVAL * args.steps,
         "clocks": clk.summary(),
         "knn_s": knn_s, "total": total,
-        "kernel_variant": {0: "generic", 1: "warp-dmma", 2: "warp-dmma+dcache"}.get(dp.kernel_variant, "?"),
+        "kernel_variant": {0: "generic", 1: "warp-dmma-allreg", 2: "warp-dmma-grouped", 3: "warp-specialised", 4: "warp-specialised+dcache"}.get(dp.kernel_variant, "?"),
     }
     if not args.no_cpu_baseline:
         ordered = data.permute(plan.permutation)

@@ -147,12 +147,14 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches);
 
 /* Plan geometry: info[0] = n, [1] = m, [2] = block_lo, [3] = block_hi,
  * [4] = first global chunk, [5] = chunk count, [6] = last kernel variant
- * (0 generic, 1 warp-DMMA, 2 warp-DMMA + distance cache), [7] = device,
+ * (0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA, 3 warp-
+ * specialised DMMA, 4 warp-specialised + distance cache), [7] = device,
  * [8] = distance cache valid.  info must hold 9 entries. */
 int vgp_plan_info(const vgp_plan* plan, int64_t* info);
 
-/* Force a kernel variant (-1 auto, 0 generic, 1 warp-DMMA (cache if built),
- * 2 warp-DMMA without the distance cache) — testing aid. */
+/* Force a kernel variant (-1 auto, 0 generic, 1 all-register warp-DMMA,
+ * 2 grouped warp-DMMA, 3 warp-specialised DMMA computing distances, 4
+ * warp-specialised DMMA streaming the distance cache) — testing aid. */
 int vgp_plan_set_variant(vgp_plan* plan, int variant);
 
 /* CUDA stream (cudaStream_t) the plan launches on, for event timing. */

@@ -188,10 +188,15 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
     VGP_CUDA_TRY(cudaMemsetAsync(p->d_scalars + 1, 0, sizeof(double), s));
   }
   if (e_hi > e_lo) {
-    bool use_dmma = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
-    if (p->force_variant == 0) use_dmma = false;
-    if (p->force_variant == 1 && !use_dmma)
-      return fail(VGP_E_UNSUPPORTED, "warp-DMMA variant does not cover this m / kernel");
+    // variants: -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped
+    // warp-DMMA, 3 warp-specialised DMMA, 4 warp-specialised + distance cache
+    const bool fast = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
+    const bool cached = p->d_dcache && p->dcache_valid;
+    int v = p->force_variant;
+    if (v < 0) v = fast ? (cached ? 4 : 3) : 0;
+    if (v > 0 && !fast)
+      return fail(VGP_E_UNSUPPORTED, "warp-DMMA variants do not cover this m / kernel");
+    if (v == 4 && !cached) return fail(VGP_E_UNSUPPORTED, "no distance cache on this plan");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
       int rc = take_event(p, &ev0);
@@ -199,19 +204,16 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
       if (rc) return rc;
       VGP_CUDA_TRY(cudaEventRecord(ev0, s));
     }
-    if (p->force_variant == 2 && !use_dmma)
-      return fail(VGP_E_UNSUPPORTED, "warp-DMMA variant does not cover this m / kernel");
-    if (use_dmma) {
-      const bool keep = p->dcache_valid;
-      if (p->force_variant == 2) p->dcache_valid = false;
-      cudaError_t err = launch_loglik_dmma(*p, cp, e_lo, e_hi, s);
-      p->dcache_valid = keep;
-      VGP_CUDA_TRY(err);
-      p->kernel_variant = (p->d_dcache && p->dcache_valid && p->force_variant != 2) ? 2 : 1;
-    } else {
+    if (v == 0) {
       VGP_CUDA_TRY(launch_loglik_generic(*p, cp, e_lo, e_hi, s));
-      p->kernel_variant = 0;
+    } else if (v == 1) {
+      VGP_CUDA_TRY(launch_loglik_dmma(*p, cp, e_lo, e_hi, s));
+    } else if (v == 2) {
+      VGP_CUDA_TRY(launch_loglik_ll(*p, cp, e_lo, e_hi, s, false));
+    } else {
+      VGP_CUDA_TRY(launch_loglik_ws(*p, cp, e_lo, e_hi, s, v == 4));
     }
+    p->kernel_variant = v;
     if (p->timing) {
       VGP_CUDA_TRY(cudaEventRecord(ev1, s));
       p->events->emplace_back(ev0, ev1);
@@ -616,8 +618,9 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 2) return fail(VGP_E_INVALID, "bad variant");
-  // 2 = warp-DMMA without the distance cache (testing aid)
+  if (!plan || variant < -1 || variant > 4) return fail(VGP_E_INVALID, "bad variant");
+  // -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
+  // 3 warp-specialised DMMA, 4 warp-specialised streaming the distance cache
   plan->p.force_variant = variant;
   return VGP_OK;
 }

@@ -1,13 +1,14 @@
 // Plan-time distance cache for the fused kernel: for every block of the
-// plan, the distances of the strictly lower part of rows 1..m of its
-// conditioning block (compact order, entry (a, b) at a (a-1)/2 + b; row m is
-// the target's cross-distances v).  Distances depend on the locations and the
+// plan, the distances of the lower triangle (with the diagonal) of rows 0..m
+// of its conditioning block, in the warp-specialised kernel's shared-memory
+// tile layout (vgp_ws_kernel.cuh: 8x8 tiles of the lower tile triangle,
+// swizzled 16-byte chunks; row m is the target's cross-distances v).  Distances depend on the locations and the
 // neighbour table only, not on theta, so an MLE loop evaluates hundreds of
 // likelihoods against one cache.  Bit-identical to the on-the-fly distances
-// of vgp_dmma_kernel.cuh (same formula), so cached and uncached evaluations
+// of vgp_ws_kernel.cuh (same formula), so cached and uncached evaluations
 // agree bit for bit.
-#include "vgp_fastmath.cuh"
 #include "vgp_internal.cuh"
+#include "vgp_ws_kernel.cuh"
 
 namespace vgp {
 namespace {
@@ -21,7 +22,6 @@ build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__
   extern __shared__ double2 sxy[];  // kWarps x (m + 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* XY = sxy + warp * (m + 1);
-  const int nent = m * (m + 1) / 2;
   for (int64_t e = e_lo + (int64_t)blockIdx.x * kWarps + warp; e < e_hi;
        e += (int64_t)gridDim.x * kWarps) {
     const int32_t* J = nbr + (e - 1 - rest_lo) * (int64_t)m;
@@ -31,21 +31,24 @@ build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__
     }
     __syncwarp();
     double* out = cache + (e - 1 - rest_lo) * cstride;
-    int a = 1, b = lane;
-    while (a <= m && b >= a) {
-      b -= a;
-      ++a;
-    }
-    for (int idx = lane; idx < nent; idx += 32) {
-      const double2 pa = XY[a], pb = XY[b];
-      const double dx = pa.x - pb.x;
-      const double dy = pa.y - pb.y;
-      out[idx] = sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000)));
-      b += 32;
-      while (a <= m && b >= a) {
-        b -= a;
-        ++a;
+    // tile (I, J), J <= I < NT, row r, column col: d(8I + r, 8J + col) on and
+    // below the diagonal for rows <= m, else 0; ws::chunk_off swizzle
+    const int nt = (m + 2 + 7) / 8;
+    const int total = ws::tidx(nt, 0) * 64;
+    for (int idx = lane; idx < total; idx += 32) {
+      const int t = idx >> 6, w = idx & 63;
+      int I = 0;
+      while (ws::tidx(I + 1, 0) <= t) ++I;
+      const int J = t - ws::tidx(I, 0);
+      const int rr = w >> 3, col = w & 7;
+      const int i = 8 * I + rr, k = 8 * J + col;
+      double d = 0.0;
+      if (k <= i && i <= m) {
+        const double dx = XY[i].x - XY[k].x;
+        const double dy = XY[i].y - XY[k].y;
+        d = sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000)));  // as vgp_ws_kernel.cuh
       }
+      out[t * 64 + ws::chunk_off(rr, col >> 1) + (col & 1)] = d;
     }
     __syncwarp();
   }
@@ -60,7 +63,7 @@ __global__ void diff_kernel(const double* __restrict__ a, const double* __restri
 
 }  // namespace
 
-int64_t dcache_stride(int m) { return ((int64_t)m * (m + 1) / 2 + 1) & ~int64_t(1); }
+int64_t dcache_stride(int m) { return (int64_t)ws::tidx((m + 2 + 7) / 8, 0) * 64; }
 
 cudaError_t launch_build_dcache(const Plan& p, cudaStream_t stream) {
   const int64_t e_lo = p.rest_lo + 1, e_hi = p.rest_hi + 1;

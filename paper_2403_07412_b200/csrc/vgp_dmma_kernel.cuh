@@ -436,8 +436,8 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
 template <int NT, int KIND, int MC>
 cudaError_t launch_c(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                      cudaStream_t stream) {
-  if (p.d_dcache && p.dcache_valid)
-    return launch<NT, KIND, MC, Occupancy<NT>::kMinCtas, true>(p, cp, e_lo, e_hi, stream);
+  // the distance cache is laid out for the grouped kernel (vgp_ll_kernel.cuh);
+  // this all-register kernel always computes distances from coordinates
   return launch<NT, KIND, MC, Occupancy<NT>::kMinCtas, false>(p, cp, e_lo, e_hi, stream);
 }
 

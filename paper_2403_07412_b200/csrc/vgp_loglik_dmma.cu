@@ -1,4 +1,4 @@
-// Dispatch for the warp-per-block DMMA kernel (vgp_dmma_kernel.cuh).
+// Dispatch for the warp-per-block DMMA kernels (vgp_ll_kernel.cuh, vgp_dmma_kernel.cuh).
 #include "vgp_internal.cuh"
 
 namespace vgp {
@@ -6,6 +6,36 @@ namespace vgp {
 cudaError_t launch_dmma_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
 cudaError_t launch_dmma_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
 cudaError_t launch_dmma_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
+
+cudaError_t launch_ll_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
+cudaError_t launch_ll_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
+cudaError_t launch_ll_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
+
+cudaError_t launch_loglik_ll(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                             cudaStream_t stream, bool cache) {
+  if (!dmma_supported(p.m, cp.kind)) return cudaErrorNotSupported;
+  if (e_hi <= e_lo) return cudaSuccess;
+  switch (cp.kind) {
+    case kMatern05: return launch_ll_kMatern05(p, cp, e_lo, e_hi, stream, cache);
+    case kMatern15: return launch_ll_kMatern15(p, cp, e_lo, e_hi, stream, cache);
+    default: return launch_ll_kMatern25(p, cp, e_lo, e_hi, stream, cache);
+  }
+}
+
+cudaError_t launch_ws_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
+cudaError_t launch_ws_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
+cudaError_t launch_ws_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
+
+cudaError_t launch_loglik_ws(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                             cudaStream_t stream, bool cache) {
+  if (!dmma_supported(p.m, cp.kind)) return cudaErrorNotSupported;
+  if (e_hi <= e_lo) return cudaSuccess;
+  switch (cp.kind) {
+    case kMatern05: return launch_ws_kMatern05(p, cp, e_lo, e_hi, stream, cache);
+    case kMatern15: return launch_ws_kMatern15(p, cp, e_lo, e_hi, stream, cache);
+    default: return launch_ws_kMatern25(p, cp, e_lo, e_hi, stream, cache);
+  }
+}
 
 bool dmma_supported(int m, int kind) {
   return m >= 1 && m + 2 <= 64 && (kind == kMatern05 || kind == kMatern15 || kind == kMatern25);

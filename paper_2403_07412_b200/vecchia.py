@@ -153,8 +153,9 @@ class DevicePlan:
         return int(self.info()[6])
 
     def set_variant(self, variant: int) -> None:
-        """-1 auto, 0 generic, 1 warp-DMMA (+ distance cache if built), 2 warp-DMMA
-        without the cache (testing aid)."""
+        """-1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
+        3 warp-specialised DMMA (distances from coordinates), 4 warp-specialised
+        streaming the distance cache (testing aid)."""
         N.check(N.lib.vgp_plan_set_variant(self.handle, int(variant)))
 
     def set_data(self, dataset: geo.Dataset) -> None:

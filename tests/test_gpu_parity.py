@@ -95,12 +95,17 @@ def _plan_from_golden(vg, z):
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
-@pytest.mark.parametrize("variant", [-1, 0])
+@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3])
 def test_loglik_vs_reference_golden(vg, name, variant):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
+    fast = (int(z["m"]) + 2 <= 64 and str(z["family"]) == "matern"
+            and float(z["theta"][2]) in (0.5, 1.5, 2.5))
+    if variant > 0 and not fast:
+        pytest.skip("warp-DMMA variants cover m + 2 <= 64 closed-form Matern only")
     plan.device_plan().set_variant(variant)
     res = vg.vecchia_loglik(data, plan, spec)
+    assert plan.device_plan().kernel_variant == (variant if variant >= 0 else (4 if fast else 0))
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL
     assert rel(res.block_first, float(z["block_first"])) <= TOL_TOTAL
     # per-block terms: ill-conditioned blocks amplify ulp-level differences
@@ -278,7 +283,7 @@ def test_distance_cache_is_bit_identical(vg, name):
     dp.set_variant(-1)
     a = vg.vecchia_loglik(data, plan, spec)
     cached = dp.info()[8] == 1
-    dp.set_variant(2)
+    dp.set_variant(3)  # same warp-specialised kernel, distances from coordinates
     b = vg.vecchia_loglik(data, plan, spec)
     dp.set_variant(-1)
     assert cached
