@@ -147,14 +147,17 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches);
 
 /* Plan geometry: info[0] = n, [1] = m, [2] = block_lo, [3] = block_hi,
  * [4] = first global chunk, [5] = chunk count, [6] = last kernel variant
- * (0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA, 3 warp-
- * specialised DMMA, 4 warp-specialised + distance cache), [7] = device,
+ * (see vgp_plan_set_variant), [7] = device,
  * [8] = distance cache valid.  info must hold 9 entries. */
 int vgp_plan_info(const vgp_plan* plan, int64_t* info);
 
-/* Force a kernel variant (-1 auto, 0 generic, 1 all-register warp-DMMA,
- * 2 grouped warp-DMMA, 3 warp-specialised DMMA computing distances, 4
- * warp-specialised DMMA streaming the distance cache) — testing aid. */
+/* Force a kernel variant — testing / benchmarking aid.  -1 auto (8 when the
+ * plan has a distance cache, else 7, for m + 2 <= 64 closed-form Matern and
+ * the Euclidean metric; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
+ * 2 grouped warp-DMMA, 3/4 warp-specialised, 5/6 warp-specialised with a
+ * diagonal-only chain, 7/8 scheduler-aware warp-specialised (default),
+ * 9/10 chain-isolated warp-specialised; even numbers >= 4 stream the
+ * plan's distance cache. */
 int vgp_plan_set_variant(vgp_plan* plan, int variant);
 
 /* CUDA stream (cudaStream_t) the plan launches on, for event timing. */

@@ -189,14 +189,18 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
   }
   if (e_hi > e_lo) {
     // variants: -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped
-    // warp-DMMA, 3 warp-specialised DMMA, 4 warp-specialised + distance cache
+    // warp-DMMA, 3 warp-specialised DMMA, 4 warp-specialised + distance cache,
+    // 5 short-critical-path warp-specialised, 6 the same + distance cache,
+    // 7 scheduler-aware warp-specialised, 8 the same + distance cache,
+    // 9 chain-isolated warp-specialised, 10 the same + distance cache
     const bool fast = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
     const bool cached = p->d_dcache && p->dcache_valid;
     int v = p->force_variant;
-    if (v < 0) v = fast ? (cached ? 4 : 3) : 0;
+    if (v < 0) v = fast ? (cached ? 8 : 7) : 0;
     if (v > 0 && !fast)
       return fail(VGP_E_UNSUPPORTED, "warp-DMMA variants do not cover this m / kernel");
-    if (v == 4 && !cached) return fail(VGP_E_UNSUPPORTED, "no distance cache on this plan");
+    if ((v == 4 || v == 6 || v == 8 || v == 10) && !cached)
+      return fail(VGP_E_UNSUPPORTED, "no distance cache on this plan");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
       int rc = take_event(p, &ev0);
@@ -210,8 +214,14 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
       VGP_CUDA_TRY(launch_loglik_dmma(*p, cp, e_lo, e_hi, s));
     } else if (v == 2) {
       VGP_CUDA_TRY(launch_loglik_ll(*p, cp, e_lo, e_hi, s, false));
-    } else {
+    } else if (v <= 4) {
       VGP_CUDA_TRY(launch_loglik_ws(*p, cp, e_lo, e_hi, s, v == 4));
+    } else if (v <= 6) {
+      VGP_CUDA_TRY(launch_loglik_ws2(*p, cp, e_lo, e_hi, s, v == 6));
+    } else if (v <= 8) {
+      VGP_CUDA_TRY(launch_loglik_ws3(*p, cp, e_lo, e_hi, s, v == 8));
+    } else {
+      VGP_CUDA_TRY(launch_loglik_ws4(*p, cp, e_lo, e_hi, s, v == 10));
     }
     p->kernel_variant = v;
     if (p->timing) {
@@ -618,7 +628,7 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 4) return fail(VGP_E_INVALID, "bad variant");
+  if (!plan || variant < -1 || variant > 10) return fail(VGP_E_INVALID, "bad variant");
   // -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
   // 3 warp-specialised DMMA, 4 warp-specialised streaming the distance cache
   plan->p.force_variant = variant;

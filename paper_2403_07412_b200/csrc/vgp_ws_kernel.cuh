@@ -36,6 +36,10 @@
 // panel runs from a side staging area.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "vgp_ll_kernel.cuh"
 
 namespace vgp {
@@ -75,13 +79,21 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int NT, int KIND, int MC, bool CACHE>
-__global__ void __launch_bounds__(kThreads, 2)
+// TRACE (profiling builds only): per-pair clock64 timeline of the first
+// kTraceBlocks blocks of CTA 0 -> trace[pair][role][block][event]
+constexpr int kTraceBlocks = 8;
+constexpr int kTraceEvents = 24;
+
+// SPLIT (experiment): CTA of 16 warps; chain of pair p = warp 4p (scheduler 0,
+// away from DMMA traffic), worker = warp 1, 2, 3, 5; the other warps exit.
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool SPLIT = false>
+__global__ void __launch_bounds__(SPLIT ? 512 : kThreads, SPLIT ? 1 : 2)
 loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
                  int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
                  double* __restrict__ rest, double* __restrict__ mu_out,
                  double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
-                 const double* __restrict__ dcache, int64_t cstride) {
+                 const double* __restrict__ dcache, int64_t cstride,
+                 long long* __restrict__ trace = nullptr, int active = kPairs) {
   constexpr int P = 8 * NT;
   const int m = MC > 0 ? MC : m_rt;
   const int NC = (m + 8) >> 3;  // tile columns holding pivots or the Schur column
@@ -89,8 +101,12 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool chain = warp < kPairs;
-  const int pr = chain ? warp : warp - kPairs;
+  bool chain = warp < kPairs;
+  int pr = chain ? warp : warp - kPairs;
+  if (SPLIT) {
+    chain = (warp & 3) == 0;
+    pr = chain ? warp >> 2 : (warp <= 3 ? warp - 1 : (warp == 5 ? 3 : -1));
+  }
   double* T = smem + kHead + pr * L.stride;  // tile triangle
   double* S = T + L.tiles;                   // last-panel staging (2 tiles)
   double* O = S + 128;                       // yJ row (row m+1)
@@ -101,14 +117,20 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
   const int lbar = 2 + 2 * pr;  // L of column c written (chain -> worker)
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) smem[i] = s2 * kExp2Table[i];
-  if (CACHE && !chain && lane == 0) mbar_init(mbar);
+  if (CACHE && !chain && pr >= 0 && lane == 0) mbar_init(mbar);
   __syncthreads();
+  if (pr < 0 || pr >= active) return;
   const double* tab = smem;
 
-  const int64_t stride = (int64_t)gridDim.x * kPairs;
-  int64_t e = e_lo + (int64_t)blockIdx.x * kPairs + pr;
+  const int64_t stride = (int64_t)gridDim.x * active;
+  int64_t e = e_lo + (int64_t)blockIdx.x * active + pr;
   const int r = lane >> 2;  // fragment row
   const int q = lane & 3;   // fragment column pair
+  int tblk = 0;
+  auto mark = [&](int ev) {
+    if (TRACE && blockIdx.x == 0 && lane == 0 && tblk < kTraceBlocks && ev < kTraceEvents)
+      trace[((pr * 2 + (chain ? 0 : 1)) * kTraceBlocks + tblk) * kTraceEvents + ev] = clock64();
+  };
 
   if (!chain) {
     // ============================ worker warp ============================
@@ -129,8 +151,9 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
     }
     int par = 0;
     bool first = true;
-    for (; e < e_hi; e += stride, par ^= 1, first = false) {
+    for (; e < e_hi; e += stride, par ^= 1, first = false, ++tblk) {
       const int64_t en = e + stride;
+      mark(0);
       // ---- this block's yJ row, target observation (and coordinates)
       if (lane < P) O[lane] = lane < m ? pf0.z : 0.0;
       if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1.z : 0.0;
@@ -166,6 +189,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
         phase ^= 1;
       }
       __syncwarp();
+      mark(1);
 
 #pragma unroll
       for (int c = 0; c < NT; ++c) {
@@ -209,6 +233,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
             for (int I = 0; I < NT; ++I)
               if (I > c) a[I] = ld2(T + tidx(I, k) * 64 + chunk_off(r, q));
             a[c] = b;
+            if (k == c - 1) mark(3 + 2 * c);
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
@@ -220,6 +245,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
 #pragma unroll
           for (int k = 0; k + 1 < c; ++k) update(k);
           if (c >= 1) {
+            mark(2 + 2 * c);
             bar_sync(lbar, 64);  // L of column c - 1 is in T
             update(c - 1);
           }
@@ -243,13 +269,14 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
             }
           }
           bar_arrive(cbar, 64);
+          mark(18 + (c == 0 ? 0 : (lastc ? 1 : 2)));
         }
       }
     }
   } else {
     // ============================ chain warp ============================
     int par = 0;
-    for (; e < e_hi; e += stride, par ^= 1) {
+    for (; e < e_hi; e += stride, par ^= 1, ++tblk) {
       int fj = -1;  // first non-positive pivot column
 #pragma unroll
       for (int c = 0; c < NT; ++c) {
@@ -258,6 +285,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
           const int R0 = 8 * c;
           const int NR = P - R0;
           const int jmax = min(8, m - R0);  // pivots in this tile column
+          mark(2 * c);
           bar_sync(cbar, 64);
           // lane owns panel rows R0 + lane + 32 rr: tile c + (lane + 32 rr) / 8, row lane & 7
           constexpr int kMaxRows = 2;
@@ -280,6 +308,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
               }
             }
           }
+          mark(2 * c + 1);  // after the first LDS behind the (deferred-blocking) barrier
           // last column: rows are in registers, S may be refilled
           if (lastc && e + stride < e_hi) bar_arrive(lbar, 64);
           double lastpiv = 1.0;
@@ -331,6 +360,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
               }
             }
             bar_arrive(lbar, 64);
+            mark(16 + (c & 1));
           } else {
             // sigma_new = A[m][m], -mu = A[m+1][m] after m pivots (vg/vecchia.py:186-189, :206)
             const int cs = m - R0;
@@ -356,6 +386,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
                 }
               }
             }
+            mark(20);
           }
         }
       }
@@ -363,36 +394,70 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
   }
 }
 
-template <int NT, int KIND, int MC, bool CACHE>
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool SPLIT = false>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, long long* trace = nullptr) {
+  constexpr int kThr = SPLIT ? 512 : kThreads;
   constexpr PairLayout L = pair_layout(NT);
   const size_t sm = sizeof(double) * ((size_t)kHead + (size_t)kPairs * L.stride);
   static size_t configured[64] = {};
   const int dev = p.device & 63;
-  auto kern = loglik_ws_kernel<NT, KIND, MC, CACHE>;
+  auto kern = loglik_ws_kernel<NT, KIND, MC, CACHE, TRACE, SPLIT>;
   if (configured[dev] < sm) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
     configured[dev] = sm;
   }
   int per_sm = 0;
-  cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, sm);
+  cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThr, sm);
   if (err != cudaSuccess) return err;
   if (per_sm < 1) per_sm = 1;
+  int active = kPairs;
+  if (TRACE) {
+    if (const char* a = std::getenv("VGP_ACTIVE")) active = std::atoi(a), per_sm = 1;
+  }
   const int64_t count = e_hi - e_lo;
-  const int64_t want = (count + kPairs - 1) / kPairs;
+  const int64_t want = (count + active - 1) / active;
   const int64_t cap = (int64_t)p.num_sms * per_sm;
   const int grid = (int)(want < cap ? want : cap);
-  kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2,
+  kern<<<grid, kThr, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2,
                                        cp.inv_beta, p.d_rest, p.d_mu, p.d_sig, p.d_fail,
-                                       p.d_dcache, p.dcache_stride);
+                                       p.d_dcache, p.dcache_stride, trace, active);
   return cudaGetLastError();
+}
+
+// VGP_TRACE=<file>: one traced launch (m = 60, nu = 1.5, cache) appends the
+// per-pair timeline of CTA 0 to <file> (tools/ws_trace.py reads it)
+inline cudaError_t launch_traced(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                                 cudaStream_t stream, const char* path) {
+  const size_t n = (size_t)kPairs * 2 * kTraceBlocks * kTraceEvents;
+  long long* d = nullptr;
+  cudaError_t err = cudaMalloc(&d, n * sizeof(long long));
+  if (err != cudaSuccess) return err;
+  cudaMemsetAsync(d, 0, n * sizeof(long long), stream);
+  const char* split = std::getenv("VGP_SPLIT");
+  if (split && split[0] == '1')
+    err = launch<8, kMatern15, 60, true, true, true>(p, cp, e_lo, e_hi, stream, d);
+  else
+    err = launch<8, kMatern15, 60, true, true>(p, cp, e_lo, e_hi, stream, d);
+  std::vector<long long> h(n);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(h.data(), d, n * sizeof(long long), cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+  cudaFree(d);
+  if (err != cudaSuccess) return err;
+  if (FILE* f = std::fopen(path, "a")) {
+    for (size_t i = 0; i < n; ++i) std::fprintf(f, "%lld%c", h[i], (i + 1) % kTraceEvents ? ' ' : '\n');
+    std::fclose(f);
+  }
+  return cudaSuccess;
 }
 
 template <int NT, int KIND, int MC>
 cudaError_t launch_c(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                      cudaStream_t stream, bool cache) {
+  if (NT == 8 && KIND == kMatern15 && MC == 60 && cache) {
+    if (const char* path = std::getenv("VGP_TRACE")) return launch_traced(p, cp, e_lo, e_hi, stream, path);
+  }
   if (cache) return launch<NT, KIND, MC, true>(p, cp, e_lo, e_hi, stream);
   return launch<NT, KIND, MC, false>(p, cp, e_lo, e_hi, stream);
 }
