@@ -146,6 +146,7 @@ void free_plan(Plan* p) {
   cudaFree(p->d_scalars);
   cudaFree(p->d_fail);
   cudaFree(p->d_work);
+  cudaFree(p->d_gscratch);
   cudaFree(p->d_dcache);
   cudaFree(p->d_prev_locs);
   cudaFree(p->d_flag);
@@ -194,12 +195,16 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
     // 7 scheduler-aware warp-specialised, 8 the same + distance cache,
     // 9 chain-isolated warp-specialised, 10 the same + distance cache
     const bool fast = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
+    const bool large = !fast && big_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN &&
+                       (!big_needs_scratch(p->m) || p->d_gscratch);
     const bool cached = p->d_dcache && p->dcache_valid;
     int v = p->force_variant;
-    if (v < 0) v = fast ? (cached ? 8 : 7) : 0;
-    if (v > 0 && !fast)
+    if (v < 0) v = fast ? (cached ? 8 : 7) : (large ? (cached ? 12 : 11) : 0);
+    if (v > 0 && v <= 10 && !fast)
       return fail(VGP_E_UNSUPPORTED, "warp-DMMA variants do not cover this m / kernel");
-    if ((v == 4 || v == 6 || v == 8 || v == 10) && !cached)
+    if (v >= 11 && !(fast || large))
+      return fail(VGP_E_UNSUPPORTED, "large-m DMMA variant does not cover this m / kernel");
+    if ((v == 4 || v == 6 || v == 8 || v == 10 || v == 12) && !cached)
       return fail(VGP_E_UNSUPPORTED, "no distance cache on this plan");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
@@ -220,8 +225,10 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
       VGP_CUDA_TRY(launch_loglik_ws2(*p, cp, e_lo, e_hi, s, v == 6));
     } else if (v <= 8) {
       VGP_CUDA_TRY(launch_loglik_ws3(*p, cp, e_lo, e_hi, s, v == 8));
-    } else {
+    } else if (v <= 10) {
       VGP_CUDA_TRY(launch_loglik_ws4(*p, cp, e_lo, e_hi, s, v == 10));
+    } else {
+      VGP_CUDA_TRY(launch_loglik_big(*p, cp, e_lo, e_hi, s, v == 12));
     }
     p->kernel_variant = v;
     if (p->timing) {
@@ -466,7 +473,7 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
       rc = dalloc(&p->d_work, p->work_doubles);
     }
   }
-  if (!rc && nrest > 0 && dmma_supported(m, kMatern15) && metric == VGP_METRIC_EUCLIDEAN) {
+  if (!rc && nrest > 0 && big_supported(m, kMatern15) && metric == VGP_METRIC_EUCLIDEAN) {
     // distance cache: on unless VGP_DCACHE=0, and only when it fits in half
     // of the free device memory
     const char* env = std::getenv("VGP_DCACHE");
@@ -489,6 +496,17 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
         p->d_flag = nullptr;
         cudaGetLastError();
       }
+    }
+  }
+  if (!rc && nrest > 0 && big_supported(m, kMatern15) && big_needs_scratch(m)) {
+    // large-m tiles: two CTA slots per SM (the scratch stays mostly in L2)
+    const int slots = p->num_sms * 2;
+    if (cudaMalloc((void**)&p->d_gscratch, sizeof(double) * (size_t)big_scratch_doubles(m) * slots) ==
+        cudaSuccess) {
+      p->gscratch_slots = slots;
+    } else {
+      p->d_gscratch = nullptr;
+      cudaGetLastError();
     }
   }
   if (!rc && cudaMallocHost((void**)&p->h_small, 64) != cudaSuccess)
@@ -628,7 +646,7 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 10) return fail(VGP_E_INVALID, "bad variant");
+  if (!plan || variant < -1 || variant > 12) return fail(VGP_E_INVALID, "bad variant");
   // -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
   // 3 warp-specialised DMMA, 4 warp-specialised streaming the distance cache
   plan->p.force_variant = variant;

@@ -1,0 +1,328 @@
+// CTA-per-block FP64 tensor-core (DMMA) Vecchia kernel for large conditioning
+// sets (m + 2 > 64; BASELINE configs 3-4: m = 90..400).
+//
+// One CTA of 4 warps owns one conditioning block e >= 1 at a time
+// (vg/vecchia.py:154-162 assemble, :180-190 _numeric_stage, :193-214
+// _reduction_stage); the augmented (8 NT)^2 matrix (rows 0..m-1 Sigma_e, row
+// m v_e, row m+1 yJ, zero padding) is factored left-looking over 8-wide tile
+// columns:
+//
+//   column   the tiles (I, c), I >= c, are dealt to the warps in groups of
+//            kGroup; each tile is generated (lean FP64 Matern) and updated
+//            with every earlier tile column's L, mma.sync.m8n8k4.f64 (SASS
+//            DMMA.8x8x4), kGroup independent accumulators per warp;
+//   diagonal warp 0 factors the 8x8 diagonal tile (one rsqrt / shuffle pivot
+//            chain) and publishes L_cc transposed + the reciprocal pivots; at
+//            the last column its panel also holds rows m, m+1, whose Schur
+//            complement gives sigma_new, -mu and the block's log-density;
+//   solve    every warp solves 32-row chunks of the rows below the diagonal
+//            tile against L_cc (row per lane, L_cc broadcast from shared
+//            memory) and writes L back in DMMA-operand order.
+//
+// Tiles live in the ws:: swizzled layout (conflict-free fragment and row
+// accesses): in shared memory while the tile triangle fits (m <= ~200,
+// several CTAs per SM overlap one block's serial diagonal phase with the
+// others' DMMA phases), otherwise in a per-CTA global scratch that stays in
+// L2.  Distances come from the plan's cache (same tile layout, read straight
+// from HBM with coalesced 512-byte tile loads) or from the gathered
+// coordinates.
+#pragma once
+
+#include "vgp_ws_kernel.cuh"
+
+namespace vgp {
+namespace big {
+
+using dmma::neg;
+using dmma::shfl;
+using ll::cov_lean;
+using ll::ld2;
+using ll::mma;
+using ll::rsqrt_chain;
+using ll::st2;
+using ws::chunk_off;
+using ws::tidx;
+
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kGroup = 4;  // tiles per warp in flight
+constexpr int kHead = 256 + 64 + 8;  // exp table | Lt | Iv
+
+__host__ __device__ inline int ntiles_of(int m) { return (m + 2 + 7) / 8; }
+// doubles of the shared-memory area besides the tiles
+__host__ __device__ inline int head_doubles(int m) { return kHead + 3 * 8 * ntiles_of(m) + 4; }
+__host__ __device__ inline int64_t tile_doubles(int m) {
+  const int nt = ntiles_of(m);
+  return (int64_t)tidx(nt, 0) * 64;
+}
+
+template <int KIND, bool CACHE, bool GT>
+__global__ void __launch_bounds__(kThreads)
+loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
+                  int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
+                  double* __restrict__ rest, double* __restrict__ mu_out,
+                  double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
+                  const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch) {
+  const int NT = ntiles_of(m);
+  const int P = 8 * NT;
+  const int NC = (m + 8) >> 3;  // tile columns holding pivots or the Schur column
+  extern __shared__ __align__(16) double smem[];
+  double* tabw = smem;
+  double* Lt = smem + 256;  // L_cc transposed: Lt[8k + j] = L[j][k]
+  double* Iv = Lt + 64;     // reciprocal pivots
+  double* O = smem + kHead;  // yJ row (row m+1)
+  double2* XY = reinterpret_cast<double2*>(O + P);
+  double* Y = O + 3 * P;  // target observation
+  double* T = GT ? gscratch + (size_t)blockIdx.x * tile_doubles(m) : smem + head_doubles(m);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2;  // fragment row
+  const int q = lane & 3;   // fragment column pair
+
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tabw[i] = s2 * kExp2Table[i];
+  __syncthreads();
+  const double* tab = smem;
+  auto tile = [&](int I, int J) -> double* { return T + (size_t)tidx(I, J) * 64; };
+
+  int fj = -1;  // warp 0: first non-positive pivot column of the current block
+  for (int64_t e = e_lo + blockIdx.x; e < e_hi; e += gridDim.x) {
+    const double* D = CACHE ? dcache + (e - 1 - rest_lo) * cstride : nullptr;
+    // ---- gather: yJ row, target observation (and coordinates)
+    for (int a = threadIdx.x; a < P; a += blockDim.x) {
+      double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (a < m) p = pts[nbr[(e - 1 - rest_lo) * (int64_t)m + a]];
+      else if (a == m) p = pts[m + e - 1];
+      O[a] = a < m ? p.z : 0.0;
+      if (a == m) Y[0] = p.z;
+      if (!CACHE) XY[a] = make_double2(p.x, p.y);
+    }
+    fj = -1;
+    __syncthreads();
+
+    for (int c = 0; c < NC; ++c) {
+      const bool lastc = (c == NC - 1);
+      // ================= column c: generate + left-looking DMMA update =================
+      for (int I0 = c + warp * kGroup; I0 < NT; I0 += kWarps * kGroup) {
+        double acc[kGroup][2];
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+          const int I = I0 + g;
+          acc[g][0] = acc[g][1] = 0.0;
+          if (I < NT) {
+            const int i = 8 * I + r;
+            double v0, v1;
+            if (CACHE) {
+              const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, c) * 64 + chunk_off(r, q)));
+              v0 = cov_lean<KIND>(dv.x, inv_beta, tab);
+              v1 = cov_lean<KIND>(dv.y, inv_beta, tab);
+            } else {
+              const double2 pa = XY[i < P ? i : 0];
+              const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * c + 2 * q);
+              double dx = pa.x - pb.x, dy = pa.y - pb.y;
+              v0 = cov_lean<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab);
+              dx = pa.x - pb.z;
+              dy = pa.y - pb.w;
+              v1 = cov_lean<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab);
+            }
+            if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
+              const double2 ov = ld2(O + 8 * c + 2 * q);
+              v0 = i == m + 1 ? ov.x : 0.0;
+              v1 = i == m + 1 ? ov.y : 0.0;
+            }
+            acc[g][0] = v0;
+            acc[g][1] = v1;
+          }
+        }
+        for (int k = 0; k < c; ++k) {
+          const double2 b = ld2(tile(c, k) + chunk_off(r, q));
+          double2 a[kGroup];
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g)
+            a[g] = I0 + g < NT ? ld2(tile(I0 + g, k) + chunk_off(r, q)) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g)
+              mma(acc[g][0], acc[g][1], neg(kk ? a[g].y : a[g].x), kk ? b.y : b.x);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g)
+          if (I0 + g < NT) st2(tile(I0 + g, c) + chunk_off(r, q), acc[g][0], acc[g][1]);
+      }
+      __syncthreads();
+
+      // ================= diagonal tile (warp 0) =================
+      if (warp == 0) {
+        const int R0 = 8 * c;
+        const int jmax = min(8, m - R0);
+        const int nrows = lastc ? P - R0 : 8;  // last column: rows m, m+1 ride along (<= 16)
+        double a[8];
+        {
+          const int I = c + (lane >> 3);
+          const double* base = tile(I < NT ? I : c, c);
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            double2 v = make_double2(0.0, 0.0);
+            if (lane < nrows) v = ld2(base + chunk_off(lane & 7, x));
+            a[2 * x] = v.x;
+            a[2 * x + 1] = v.y;
+          }
+        }
+        double lastpiv = 1.0;
+        double iv[8];
+        if (jmax > 0) {
+          double piv = shfl(a[0], 0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < jmax) {
+              if (j == jmax - 1) lastpiv = piv;
+              const double inv = rsqrt_chain(piv);
+              iv[j] = inv;
+              a[j] *= inv;
+              if (j + 1 < 8) {
+                const double nxt = fma(-a[j], a[j], a[j + 1]);
+                piv = shfl(nxt, j + 1);
+              }
+#pragma unroll
+              for (int jp = j + 1; jp < 8; ++jp) {
+                const double lc = shfl(a[j], jp);  // L[R0 + jp][R0 + j]
+                a[jp] = fma(-a[j], lc, a[jp]);
+              }
+            }
+          }
+        }
+        // pivot test !(piv > 0) (vg/batchla.py:146-151): a non-positive or NaN
+        // pivot turns every later pivot NaN; locate the first bad column
+        if (!(lastpiv > 0.0) && fj < 0) {
+          double ljj = a[0];
+#pragma unroll
+          for (int x = 1; x < 8; ++x)
+            if (lane == x) ljj = a[x];
+          const unsigned bad = __ballot_sync(0xffffffffu, lane < jmax && !(ljj > 0.0));
+          fj = R0 + (bad ? __ffs(bad) - 1 : jmax - 1);
+        }
+        if (!lastc) {
+#pragma unroll
+          for (int k = 0; k < 7; ++k)
+            if (lane > k && lane < 8) Lt[8 * k + lane] = a[k];
+          if (lane == 0) {
+            st2(Iv, iv[0], iv[1]);
+            st2(Iv + 2, iv[2], iv[3]);
+            st2(Iv + 4, iv[4], iv[5]);
+            st2(Iv + 6, iv[6], iv[7]);
+          }
+        } else {
+          // sigma_new = A[m][m], -mu = A[m+1][m] after m pivots (vg/vecchia.py:186-189, :206)
+          const int cs = m - R0;
+          double v = a[0];
+#pragma unroll
+          for (int x = 1; x < 8; ++x)
+            if (x == cs) v = a[x];
+          const double sg = shfl(v, cs);
+          const double mu = -shfl(v, cs + 1);
+          if (lane == 0) {
+            const int64_t kk = e - 1 - rest_lo;
+            if (fj >= 0) {
+              atomicMin(&fail[0], npd_key(e, fj, m));
+            } else {
+              mu_out[kk] = mu;
+              sig_out[kk] = sg;
+              if (!(sg > 0.0)) {
+                atomicMin(&fail[1], (unsigned long long)e);
+                rest[kk] = 0.0;
+              } else {
+                const double resid = Y[0] - mu;
+                rest[kk] = -0.5 * (resid * resid / sg + kLog2Pi + log(sg));
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (lastc) break;
+
+      // ================= solve the rows below the diagonal tile =================
+      {
+        const double2 i01 = ld2(Iv), i23 = ld2(Iv + 2), i45 = ld2(Iv + 4), i67 = ld2(Iv + 6);
+        const double iv[8] = {i01.x, i01.y, i23.x, i23.y, i45.x, i45.y, i67.x, i67.y};
+        for (int rb = 8 * (c + 1) + 32 * warp; rb < P; rb += 32 * kWarps) {
+          const int row = rb + lane;
+          const bool ok = row < P;
+          double* base = tile(ok ? row >> 3 : c + 1, c);
+          double a[8];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            double2 v = make_double2(0.0, 0.0);
+            if (ok) v = ld2(base + chunk_off(lane & 7, x));
+            a[2 * x] = v.x;
+            a[2 * x + 1] = v.y;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            a[k] *= iv[k];
+            if (k + 1 < 8) {
+              double lt[8];
+#pragma unroll
+              for (int x = (k + 1) & ~1; x < 8; x += 2) {
+                const double2 v = ld2(Lt + 8 * k + x);
+                lt[x] = v.x;
+                lt[x + 1] = v.y;
+              }
+#pragma unroll
+              for (int j = k + 1; j < 8; ++j) a[j] = fma(-a[k], lt[j], a[j]);
+            }
+          }
+          if (ok) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) st2(base + chunk_off(lane & 7, x), a[x], a[x + 4]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+inline size_t smem_bytes(int m, bool gt) {
+  return sizeof(double) * ((size_t)head_doubles(m) + (gt ? 0 : (size_t)tile_doubles(m)));
+}
+// tiles in shared memory up to ~200 KB per CTA, else the global scratch
+inline bool use_global_tiles(int m) { return smem_bytes(m, false) > 200 * 1024; }
+
+template <int KIND, bool CACHE, bool GT>
+cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                   cudaStream_t stream, double* gscratch, int max_grid) {
+  const size_t sm = smem_bytes(p.m, GT);
+  auto kern = loglik_big_kernel<KIND, CACHE, GT>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (err != cudaSuccess) return err;
+  int per_sm = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, sm);
+  if (err != cudaSuccess) return err;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t count = e_hi - e_lo;
+  int64_t cap = (int64_t)p.num_sms * per_sm;
+  if (GT && cap > max_grid) cap = max_grid;
+  const int grid = (int)(count < cap ? count : cap);
+  kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2,
+                                       cp.inv_beta, p.d_rest, p.d_mu, p.d_sig, p.d_fail,
+                                       p.d_dcache, p.dcache_stride, gscratch);
+  return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                        cudaStream_t stream, bool cache, double* gscratch, int max_grid) {
+  const bool gt = use_global_tiles(p.m);
+  if (gt && !gscratch) return cudaErrorInvalidValue;
+  if (cache) {
+    return gt ? launch<KIND, true, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
+              : launch<KIND, true, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  }
+  return gt ? launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
+            : launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+}
+
+}  // namespace big
+}  // namespace vgp

@@ -86,7 +86,9 @@ struct Plan {
   int kernel_variant = -1;      // last kernel used (for introspection)
   int force_variant = -1;       // -1 auto
   int tune = 0;                 // experiment selector (env VGP_TUNE at plan creation)
-  double* d_dcache = nullptr;   // per-block distance cache (compact lower rows 1..m)
+  double* d_gscratch = nullptr; // large-m kernel: per-CTA tile triangles (L2-resident)
+  int gscratch_slots = 0;
+  double* d_dcache = nullptr;   // per-block distance cache (ws:: tile layout)
   int64_t dcache_stride = 0;    // doubles per block (16-byte multiple)
   bool dcache_valid = false;
   double* d_prev_locs = nullptr;  // locations the cache was built from (n x 2)
@@ -124,6 +126,13 @@ cudaError_t launch_loglik_ll(const Plan& p, const CovParams& cp, int64_t e_lo, i
 // coverage; `cache` streams the plan's distance cache (vgp_dcache.cu).
 cudaError_t launch_loglik_ws(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                              cudaStream_t stream, bool cache);
+// Large-m CTA-per-block DMMA kernel (vgp_big_kernel.cuh), any m with a
+// closed-form Matern; tiles in shared memory or, past ~200 KB, in d_gscratch.
+bool big_supported(int m, int kind);
+bool big_needs_scratch(int m);
+int64_t big_scratch_doubles(int m);
+cudaError_t launch_loglik_big(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                              cudaStream_t stream, bool cache);
 // Short-critical-path variant: the chain warp factors only the diagonal
 // tiles, the worker solves the rows below and hands the next diagonal tile
 // over first (vgp_ws2_kernel.cuh); same cache layout.

@@ -95,17 +95,21 @@ def _plan_from_golden(vg, z):
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
-@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 def test_loglik_vs_reference_golden(vg, name, variant):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
-    fast = (int(z["m"]) + 2 <= 64 and str(z["family"]) == "matern"
-            and float(z["theta"][2]) in (0.5, 1.5, 2.5))
-    if variant > 0 and not fast:
+    closed = (str(z["family"]) == "matern" and float(z["theta"][2]) in (0.5, 1.5, 2.5)
+              and str(z.get("metric", "euclidean")) == "euclidean")
+    fast = closed and int(z["m"]) + 2 <= 64
+    if 0 < variant <= 10 and not fast:
         pytest.skip("warp-DMMA variants cover m + 2 <= 64 closed-form Matern only")
+    if variant >= 11 and not closed:
+        pytest.skip("the large-m DMMA kernel covers closed-form Matern only")
     plan.device_plan().set_variant(variant)
     res = vg.vecchia_loglik(data, plan, spec)
-    assert plan.device_plan().kernel_variant == (variant if variant >= 0 else (8 if fast else 0))
+    auto = 8 if fast else (12 if closed else 0)
+    assert plan.device_plan().kernel_variant == (variant if variant >= 0 else auto)
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL
     assert rel(res.block_first, float(z["block_first"])) <= TOL_TOTAL
     # per-block terms: ill-conditioned blocks amplify ulp-level differences
