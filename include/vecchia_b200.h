@@ -109,6 +109,13 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
  * the device (Dataset.permute, vg/geo.py:145-149). */
 int vgp_plan_set_data(vgp_plan* plan, const double* locations, const double* observations);
 
+/* Page-lock a host range so uploads from it (vgp_plan_set_data) and result
+ * downloads into it run as asynchronous DMA (cudaHostRegister); the Python
+ * package registers a dataset's arrays on first use and unregisters them when
+ * they are freed.  No reference counterpart (host-side transfer plumbing). */
+int vgp_host_register(void* ptr, int64_t bytes);
+int vgp_host_unregister(void* ptr);
+
 int vgp_plan_destroy(vgp_plan* plan);
 
 /* Replaces vecchia.vecchia_loglik (vg/vecchia.py:217-238) for a plan that

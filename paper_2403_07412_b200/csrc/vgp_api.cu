@@ -164,6 +164,11 @@ void free_plan(Plan* p) {
     delete p->event_pool;
   }
   if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  for (auto ev : p->ev_chunk)
+    if (ev) cudaEventDestroy(ev);
   delete p;
 }
 
@@ -177,13 +182,34 @@ int take_event(Plan* p, cudaEvent_t* ev) {
   return VGP_OK;
 }
 
-// Launch the full evaluation sequence on the plan's stream.
-int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
+// Host destinations of the per-block results (vgp_loglik); null = none.
+struct HostOut {
+  double* rest = nullptr;
+  double* mu = nullptr;
+  double* sig = nullptr;
+};
+
+// Launch the full evaluation sequence on the plan's stream.  The joint block
+// (entry 0, generic kernel) runs on the side stream next to the main kernel.
+// With host outputs the main kernel is launched in chunks of blocks and each
+// chunk's results are downloaded (side stream) while later chunks compute;
+// the caller synchronises both streams.
+int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* out = nullptr) {
   cudaStream_t s = p->stream;
   VGP_CUDA_TRY(cudaMemsetAsync(p->d_fail, 0xff, 2 * sizeof(unsigned long long), s));
   int64_t e_lo = p->blk_lo, e_hi = p->blk_hi;
-  if (e_lo == 0) {
+  const bool joint = e_lo == 0;
+  // the generic kernel's global workspace slots are per CTA: when the main
+  // launch may use them too, the joint block runs first on the main stream
+  const bool serial_joint = p->d_work != nullptr;
+  if (joint && serial_joint) {
     VGP_CUDA_TRY(launch_loglik_generic(*p, cp, 0, 1, s));
+    e_lo = 1;
+  } else if (joint) {
+    VGP_CUDA_TRY(cudaEventRecord(p->ev_fork, s));
+    VGP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    VGP_CUDA_TRY(launch_loglik_generic(*p, cp, 0, 1, p->side));
+    VGP_CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
     e_lo = 1;
   } else {
     VGP_CUDA_TRY(cudaMemsetAsync(p->d_scalars + 1, 0, sizeof(double), s));
@@ -193,7 +219,8 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
     // warp-DMMA, 3 warp-specialised DMMA, 4 warp-specialised + distance cache,
     // 5 short-critical-path warp-specialised, 6 the same + distance cache,
     // 7 scheduler-aware warp-specialised, 8 the same + distance cache,
-    // 9 chain-isolated warp-specialised, 10 the same + distance cache
+    // 9 chain-isolated warp-specialised, 10 the same + distance cache,
+    // 11 large-m CTA-per-block, 12 the same + distance cache
     const bool fast = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
     const bool large = !fast && big_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN &&
                        (!big_needs_scratch(p->m) || p->d_gscratch);
@@ -213,29 +240,45 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total) {
       if (rc) return rc;
       VGP_CUDA_TRY(cudaEventRecord(ev0, s));
     }
-    if (v == 0) {
-      VGP_CUDA_TRY(launch_loglik_generic(*p, cp, e_lo, e_hi, s));
-    } else if (v == 1) {
-      VGP_CUDA_TRY(launch_loglik_dmma(*p, cp, e_lo, e_hi, s));
-    } else if (v == 2) {
-      VGP_CUDA_TRY(launch_loglik_ll(*p, cp, e_lo, e_hi, s, false));
-    } else if (v <= 4) {
-      VGP_CUDA_TRY(launch_loglik_ws(*p, cp, e_lo, e_hi, s, v == 4));
-    } else if (v <= 6) {
-      VGP_CUDA_TRY(launch_loglik_ws2(*p, cp, e_lo, e_hi, s, v == 6));
-    } else if (v <= 8) {
-      VGP_CUDA_TRY(launch_loglik_ws3(*p, cp, e_lo, e_hi, s, v == 8));
-    } else if (v <= 10) {
-      VGP_CUDA_TRY(launch_loglik_ws4(*p, cp, e_lo, e_hi, s, v == 10));
-    } else {
-      VGP_CUDA_TRY(launch_loglik_big(*p, cp, e_lo, e_hi, s, v == 12));
+    auto main_kernel = [&](int64_t lo, int64_t hi) -> cudaError_t {
+      if (v == 0) return launch_loglik_generic(*p, cp, lo, hi, s);
+      if (v == 1) return launch_loglik_dmma(*p, cp, lo, hi, s);
+      if (v == 2) return launch_loglik_ll(*p, cp, lo, hi, s, false);
+      if (v <= 4) return launch_loglik_ws(*p, cp, lo, hi, s, v == 4);
+      if (v <= 6) return launch_loglik_ws2(*p, cp, lo, hi, s, v == 6);
+      if (v <= 8) return launch_loglik_ws3(*p, cp, lo, hi, s, v == 8);
+      if (v <= 10) return launch_loglik_ws4(*p, cp, lo, hi, s, v == 10);
+      return launch_loglik_big(*p, cp, lo, hi, s, v == 12);
+    };
+    const int64_t count = e_hi - e_lo;
+    const int nchunk = (out && count >= 65536) ? 4 : 1;
+    // all chunks are queued before any download: a download into pageable
+    // memory blocks the host, the later chunks keep the GPU busy meanwhile
+    for (int k = 0; k < nchunk; ++k) {
+      VGP_CUDA_TRY(main_kernel(e_lo + count * k / nchunk, e_lo + count * (k + 1) / nchunk));
+      if (out) VGP_CUDA_TRY(cudaEventRecord(p->ev_chunk[k], s));
     }
     p->kernel_variant = v;
     if (p->timing) {
       VGP_CUDA_TRY(cudaEventRecord(ev1, s));
       p->events->emplace_back(ev0, ev1);
     }
+    for (int k = 0; out && k < nchunk; ++k) {
+      const int64_t lo = e_lo + count * k / nchunk, hi = e_lo + count * (k + 1) / nchunk;
+      VGP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_chunk[k], 0));
+      const int64_t r0 = lo - 1 - p->rest_lo, nr = hi - lo;
+      if (out->rest)
+        VGP_CUDA_TRY(cudaMemcpyAsync(out->rest + r0, p->d_rest + r0, sizeof(double) * nr,
+                                     cudaMemcpyDeviceToHost, p->side));
+      if (out->mu)
+        VGP_CUDA_TRY(cudaMemcpyAsync(out->mu + r0, p->d_mu + r0, sizeof(double) * nr,
+                                     cudaMemcpyDeviceToHost, p->side));
+      if (out->sig)
+        VGP_CUDA_TRY(cudaMemcpyAsync(out->sig + r0, p->d_sig + r0, sizeof(double) * nr,
+                                     cudaMemcpyDeviceToHost, p->side));
+    }
   }
+  if (joint && !serial_joint) VGP_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
   VGP_CUDA_TRY(launch_reduce(*p, want_total, s));
   return VGP_OK;
 }
@@ -446,6 +489,11 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
   p->event_pool = new std::vector<cudaEvent_t>();
   const int64_t nrest = p->rest_hi - p->rest_lo;
   cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&p->ev_chunk[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     free_plan(p);
     return fail(VGP_E_CUDA, cudaGetErrorString(e));
@@ -541,6 +589,18 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
   h->p = *p;
   delete p;  // ownership of the device buffers moved into h->p
   *out = h;
+  return VGP_OK;
+}
+
+int vgp_host_register(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return fail(VGP_E_INVALID, "bad host range");
+  VGP_CUDA_TRY(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault));
+  return VGP_OK;
+}
+
+int vgp_host_unregister(void* ptr) {
+  if (!ptr) return fail(VGP_E_INVALID, "null pointer");
+  VGP_CUDA_TRY(cudaHostUnregister(ptr));
   return VGP_OK;
 }
 
@@ -695,23 +755,19 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
   int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
   if (rc) return rc;
   DeviceGuard g(p->device);
-  rc = launch_eval(p, cp, true);
+  HostOut out;
+  out.rest = block_rest;
+  out.mu = mu_new;
+  out.sig = sigma_new;
+  const bool any = block_rest || mu_new || sigma_new;
+  rc = launch_eval(p, cp, true, any ? &out : nullptr);
   if (rc) return rc;
-  const int64_t nrest = p->rest_hi - p->rest_lo;
   unsigned long long* flags = (unsigned long long*)p->h_small;
   double* sc = p->h_small + 2;
   VGP_CUDA_TRY(cudaMemcpyAsync(flags, p->d_fail, 2 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, p->stream));
   VGP_CUDA_TRY(cudaMemcpyAsync(sc, p->d_scalars, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
-  if (block_rest)
-    VGP_CUDA_TRY(cudaMemcpyAsync(block_rest, p->d_rest, sizeof(double) * nrest,
-                                 cudaMemcpyDeviceToHost, p->stream));
-  if (mu_new)
-    VGP_CUDA_TRY(cudaMemcpyAsync(mu_new, p->d_mu, sizeof(double) * nrest, cudaMemcpyDeviceToHost,
-                                 p->stream));
-  if (sigma_new)
-    VGP_CUDA_TRY(cudaMemcpyAsync(sigma_new, p->d_sig, sizeof(double) * nrest,
-                                 cudaMemcpyDeviceToHost, p->stream));
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->side));
   VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
   int st = decode_status(p, flags, fail_index);
   if (total) *total = st == VGP_OK ? sc[0] : NAN;

@@ -65,6 +65,9 @@ struct Plan {
   int64_t blk_lo = 0, blk_hi = 0;  // batch entries [blk_lo, blk_hi); entry 0 = joint block
   int64_t rest_lo = 0, rest_hi = 0;  // block_rest indices k = e - 1 covered by this plan
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // joint block and result downloads overlap the main kernel
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_chunk[8] = {};
   int64_t* d_order = nullptr;   // n, ordered position -> original index
   int32_t* d_nbr = nullptr;     // (rest_hi - rest_lo) x m, row r <-> entry rest_lo + r + 1
   double4* d_pts = nullptr;     // n x (x, y, obs, 0), ordered

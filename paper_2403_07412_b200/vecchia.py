@@ -164,6 +164,9 @@ class DevicePlan:
             raise ValueError(f"plan built for n={self.n}, dataset has n={dataset.n}")
         locs = np.ascontiguousarray(dataset.locations, dtype=np.float64)
         obs = np.ascontiguousarray(dataset.observations, dtype=np.float64)
+        if locs is dataset.locations and obs is dataset.observations:
+            _pin(locs)
+            _pin(obs)
         N.check(N.lib.vgp_plan_set_data(self.handle, N.dptr(locs), N.dptr(obs)))
 
     @property
@@ -237,6 +240,29 @@ class DevicePlan:
         st = ctypes.c_int(0)
         N.check(N.lib.vgp_plan_fetch(self.handle, N.dptr(total), N.iptr(fail), ctypes.byref(st)))
         return float(total[0]), int(st.value), int(fail[0])
+
+
+_PINNED: dict = {}  # data pointer -> bytes of page-locked dataset arrays
+
+
+def _pin(arr: np.ndarray) -> None:
+    """Page-lock a dataset array in place the first time it is uploaded, so
+    the per-evaluation upload runs as DMA; unregistered when the array is
+    freed.  Registration failure leaves the (slower) pageable upload."""
+    if not arr.flags.owndata or arr.nbytes < (1 << 20):
+        return
+    ptr = arr.ctypes.data
+    if ptr in _PINNED:
+        return
+    if N.lib.vgp_host_register(ctypes.c_void_p(ptr), arr.nbytes) != 0:
+        return
+    _PINNED[ptr] = arr.nbytes
+    weakref.finalize(arr, _unpin, ptr)
+
+
+def _unpin(ptr: int) -> None:
+    if _PINNED.pop(ptr, None) is not None:
+        N.lib.vgp_host_unregister(ctypes.c_void_p(ptr))
 
 
 class LikelihoodSession:

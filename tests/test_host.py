@@ -157,3 +157,15 @@ def test_exact_objective_is_out_of_scope():
     data = vg.Dataset(np.random.default_rng(0).random((40, 2)), np.zeros(40))
     with pytest.raises(NotImplementedError):
         vg.mle_estimate(data, vg.FitConfig(objective="exact"))
+
+
+def test_pin_skips_views_and_small_arrays():
+    """Only arrays that own at least 1 MiB of data are page-locked (views and
+    small arrays keep the pageable upload), and nothing is registered twice."""
+    V = vecchia
+    before = dict(V._PINNED)
+    small = np.zeros(100)
+    V._pin(small)
+    view = np.zeros((300000, 2))[:, :1]
+    V._pin(view)
+    assert V._PINNED == before
