@@ -4,7 +4,7 @@
 namespace vgp {
 
 bool big_supported(int m, int kind) {
-  return m >= 1 && m <= 4096 && (kind == kMatern05 || kind == kMatern15 || kind == kMatern25);
+  return m >= 1 && m <= 4096;  // every kernel family (vg/kernels.py:59-91)
 }
 
 bool big_needs_scratch(int m) { return big::use_global_tiles(m); }
@@ -19,8 +19,12 @@ cudaError_t launch_loglik_big(const Plan& p, const CovParams& cp, int64_t e_lo, 
       return big::launch_kind<kMatern05>(p, cp, e_lo, e_hi, stream, cache, p.d_gscratch, p.gscratch_slots);
     case kMatern15:
       return big::launch_kind<kMatern15>(p, cp, e_lo, e_hi, stream, cache, p.d_gscratch, p.gscratch_slots);
-    default:
+    case kMatern25:
       return big::launch_kind<kMatern25>(p, cp, e_lo, e_hi, stream, cache, p.d_gscratch, p.gscratch_slots);
+    case kMaternGen:
+      return big::launch_kind<kMaternGen>(p, cp, e_lo, e_hi, stream, cache, p.d_gscratch, p.gscratch_slots);
+    default:
+      return big::launch_kind<kPowExp>(p, cp, e_lo, e_hi, stream, cache, p.d_gscratch, p.gscratch_slots);
   }
 }
 

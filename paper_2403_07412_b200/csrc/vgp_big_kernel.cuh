@@ -28,6 +28,7 @@
 // coordinates.
 #pragma once
 
+#include "vgp_math.cuh"
 #include "vgp_ws_kernel.cuh"
 
 namespace vgp {
@@ -56,15 +57,26 @@ __host__ __device__ inline int64_t tile_doubles(int m) {
   return (int64_t)tidx(nt, 0) * 64;
 }
 
+// covariance at distance d: lean closed forms, or the reference expression
+// (general-nu Matern via the device Bessel K_nu, power exponential;
+// vg/kernels.py:59-91) with C(0) = sigma^2 exactly (d below 1e-100: the
+// diagonal and exact duplicates, whose distance is 2^-500 by construction)
+template <int KIND>
+__device__ __forceinline__ double cov_any(double d, const CovParams& cp, const double* tab) {
+  if (KIND <= kMatern25) return cov_lean<KIND>(d, cp.inv_beta, tab);
+  return d < 1e-100 ? cp.s2 : cov_ref(cp, d);
+}
+
 template <int KIND, bool CACHE, bool GT>
 __global__ void __launch_bounds__(kThreads)
 loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
-                  int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
+                  int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
                   const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch) {
   const int NT = ntiles_of(m);
   const int P = 8 * NT;
+  const double s2 = cp.s2;
   const int NC = (m + 8) >> 3;  // tile columns holding pivots or the Schur column
   extern __shared__ __align__(16) double smem[];
   double* tabw = smem;
@@ -113,16 +125,16 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             double v0, v1;
             if (CACHE) {
               const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, c) * 64 + chunk_off(r, q)));
-              v0 = cov_lean<KIND>(dv.x, inv_beta, tab);
-              v1 = cov_lean<KIND>(dv.y, inv_beta, tab);
+              v0 = cov_any<KIND>(dv.x, cp, tab);
+              v1 = cov_any<KIND>(dv.y, cp, tab);
             } else {
               const double2 pa = XY[i < P ? i : 0];
               const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * c + 2 * q);
               double dx = pa.x - pb.x, dy = pa.y - pb.y;
-              v0 = cov_lean<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab);
+              v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab);
               dx = pa.x - pb.z;
               dy = pa.y - pb.w;
-              v1 = cov_lean<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab);
+              v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab);
             }
             if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
               const double2 ov = ld2(O + 8 * c + 2 * q);
@@ -305,8 +317,8 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   int64_t cap = (int64_t)p.num_sms * per_sm;
   if (GT && cap > max_grid) cap = max_grid;
   const int grid = (int)(count < cap ? count : cap);
-  kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2,
-                                       cp.inv_beta, p.d_rest, p.d_mu, p.d_sig, p.d_fail,
+  kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp,
+                                       p.d_rest, p.d_mu, p.d_sig, p.d_fail,
                                        p.d_dcache, p.dcache_stride, gscratch);
   return cudaGetLastError();
 }

@@ -129,8 +129,9 @@ cudaError_t launch_loglik_ll(const Plan& p, const CovParams& cp, int64_t e_lo, i
 // coverage; `cache` streams the plan's distance cache (vgp_dcache.cu).
 cudaError_t launch_loglik_ws(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                              cudaStream_t stream, bool cache);
-// Large-m CTA-per-block DMMA kernel (vgp_big_kernel.cuh), any m with a
-// closed-form Matern; tiles in shared memory or, past ~200 KB, in d_gscratch.
+// CTA-per-block DMMA kernel (vgp_big_kernel.cuh): any m, every kernel family
+// (general nu via the device Bessel K); tiles in shared memory or, past
+// ~200 KB, in d_gscratch.
 bool big_supported(int m, int kind);
 bool big_needs_scratch(int m);
 int64_t big_scratch_doubles(int m);

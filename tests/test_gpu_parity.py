@@ -104,11 +104,9 @@ def test_loglik_vs_reference_golden(vg, name, variant):
     fast = closed and int(z["m"]) + 2 <= 64
     if 0 < variant <= 10 and not fast:
         pytest.skip("warp-DMMA variants cover m + 2 <= 64 closed-form Matern only")
-    if variant >= 11 and not closed:
-        pytest.skip("the large-m DMMA kernel covers closed-form Matern only")
     plan.device_plan().set_variant(variant)
     res = vg.vecchia_loglik(data, plan, spec)
-    auto = 8 if fast else (12 if closed else 0)
+    auto = 8 if fast else 12
     assert plan.device_plan().kernel_variant == (variant if variant >= 0 else auto)
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL
     assert rel(res.block_first, float(z["block_first"])) <= TOL_TOTAL
