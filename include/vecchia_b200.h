@@ -161,9 +161,9 @@ int vgp_plan_info(const vgp_plan* plan, int64_t* info);
 /* Force a kernel variant — testing / benchmarking aid.  -1 auto (8 when the
  * plan has a distance cache, else 7, for m + 2 <= 64 closed-form Matern and
  * the Euclidean metric; 12 / 11 for larger m; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
- * 2 grouped warp-DMMA, 3/4 warp-specialised, 5/6 warp-specialised with a
- * diagonal-only chain, 7/8 scheduler-aware warp-specialised (default),
- * 9/10 chain-isolated warp-specialised, 11/12 the CTA-per-block large-m
+ * 2 grouped warp-DMMA, 3/4 warp-specialised, 7/8 scheduler-aware
+ * warp-specialised (default; 5, 6, 9, 10 are retired experiments returning
+ * VGP_E_CUDA), 11/12 the CTA-per-block large-m
  * DMMA kernel (any m, auto for m + 2 > 64 closed-form Matern); even numbers
  * >= 4 stream the plan's distance cache. */
 int vgp_plan_set_variant(vgp_plan* plan, int variant);

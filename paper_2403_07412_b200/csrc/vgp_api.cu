@@ -217,9 +217,8 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
   if (e_hi > e_lo) {
     // variants: -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped
     // warp-DMMA, 3 warp-specialised DMMA, 4 warp-specialised + distance cache,
-    // 5 short-critical-path warp-specialised, 6 the same + distance cache,
+    // (5, 6, 9, 10: retired experiments),
     // 7 scheduler-aware warp-specialised, 8 the same + distance cache,
-    // 9 chain-isolated warp-specialised, 10 the same + distance cache,
     // 11 large-m CTA-per-block, 12 the same + distance cache
     const bool fast = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
     const bool large = !fast && big_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN &&
@@ -245,9 +244,8 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
       if (v == 1) return launch_loglik_dmma(*p, cp, lo, hi, s);
       if (v == 2) return launch_loglik_ll(*p, cp, lo, hi, s, false);
       if (v <= 4) return launch_loglik_ws(*p, cp, lo, hi, s, v == 4);
-      if (v <= 6) return launch_loglik_ws2(*p, cp, lo, hi, s, v == 6);
+      if (v <= 6 || v >= 9 && v <= 10) return cudaErrorNotSupported;  // retired variants
       if (v <= 8) return launch_loglik_ws3(*p, cp, lo, hi, s, v == 8);
-      if (v <= 10) return launch_loglik_ws4(*p, cp, lo, hi, s, v == 10);
       return launch_loglik_big(*p, cp, lo, hi, s, v == 12);
     };
     const int64_t count = e_hi - e_lo;

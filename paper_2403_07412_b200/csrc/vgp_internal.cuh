@@ -137,18 +137,9 @@ bool big_needs_scratch(int m);
 int64_t big_scratch_doubles(int m);
 cudaError_t launch_loglik_big(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream, bool cache);
-// Short-critical-path variant: the chain warp factors only the diagonal
-// tiles, the worker solves the rows below and hands the next diagonal tile
-// over first (vgp_ws2_kernel.cuh); same cache layout.
-cudaError_t launch_loglik_ws2(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                              cudaStream_t stream, bool cache);
 // Scheduler-aware layout: one worker warp per SM sub-partition serving the
 // two blocks whose chain warps share that sub-partition (vgp_ws3_kernel.cuh).
 cudaError_t launch_loglik_ws3(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                              cudaStream_t stream, bool cache);
-// Pivot chains isolated on sub-partition 0 (two blocks per chain warp), DMMA
-// workers on sub-partitions 1..3 (vgp_ws4_kernel.cuh).
-cudaError_t launch_loglik_ws4(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream, bool cache);
 
 // Scatter the shard's chunk partials (and block_first) into a global device

@@ -95,7 +95,7 @@ def _plan_from_golden(vg, z):
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
-@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12])
+@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 7, 8, 11, 12])
 def test_loglik_vs_reference_golden(vg, name, variant):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
@@ -287,17 +287,13 @@ def test_distance_cache_is_bit_identical(vg, name):
     cached = dp.info()[8] == 1
     dp.set_variant(3)  # same warp-specialised kernel, distances from coordinates
     b = vg.vecchia_loglik(data, plan, spec)
-    dp.set_variant(6)
-    c = vg.vecchia_loglik(data, plan, spec)
-    dp.set_variant(5)
-    d = vg.vecchia_loglik(data, plan, spec)
     dp.set_variant(8)
     f = vg.vecchia_loglik(data, plan, spec)
     dp.set_variant(7)
     g = vg.vecchia_loglik(data, plan, spec)
-    dp.set_variant(10)
+    dp.set_variant(12)
     h = vg.vecchia_loglik(data, plan, spec)
-    dp.set_variant(9)
+    dp.set_variant(11)
     k = vg.vecchia_loglik(data, plan, spec)
     dp.set_variant(-1)
     assert cached
@@ -307,8 +303,6 @@ def test_distance_cache_is_bit_identical(vg, name):
     np.testing.assert_array_equal(f.block_rest, g.block_rest)
     assert a.total == b.total
     np.testing.assert_array_equal(a.block_rest, b.block_rest)
-    assert c.total == d.total
-    np.testing.assert_array_equal(c.block_rest, d.block_rest)
 
 
 def test_distance_cache_rebuilt_when_locations_change(vg, oracle):
