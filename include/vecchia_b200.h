@@ -109,6 +109,19 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
  * the device (Dataset.permute, vg/geo.py:145-149). */
 int vgp_plan_set_data(vgp_plan* plan, const double* locations, const double* observations);
 
+/* Kriging at test locations from m nearest training points — replaces the
+ * neighbour branch of fit.krige_predict (vg/fit.py:241-264: batch_potrf, two
+ * batch_trsv, two batch_dot per test point) with one fused kernel launch.
+ * neighbors: n_test x m training indices (geo.nearest_points, e.g. from
+ * vgp_knn_points).  Writes the conditional means (predictions) and variances
+ * sigma^2 - v'v'.  Returns VGP_NOT_POSITIVE_DEFINITE with *fail_index = the
+ * test point whose conditioning matrix has a non-positive pivot.  Euclidean
+ * metric. */
+int vgp_krige(int device, const double* train_locations, const double* train_observations,
+              int64_t n_train, const double* test_locations, int64_t n_test, int32_t m,
+              const int64_t* neighbors, int family, double sigma_sq, double beta, double nu,
+              double* predictions, double* variances, int64_t* fail_index);
+
 /* Page-lock a host range so uploads from it (vgp_plan_set_data) and result
  * downloads into it run as asynchronous DMA (cudaHostRegister); the Python
  * package registers a dataset's arrays on first use and unregisters them when

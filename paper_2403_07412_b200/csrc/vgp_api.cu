@@ -590,6 +590,111 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
   return VGP_OK;
 }
 
+int vgp_krige(int device, const double* train_locations, const double* train_observations,
+              int64_t n_train, const double* test_locations, int64_t n_test, int32_t m,
+              const int64_t* neighbors, int family, double sigma_sq, double beta, double nu,
+              double* predictions, double* variances, int64_t* fail_index) {
+  if (fail_index) *fail_index = -1;
+  if (!train_locations || !train_observations || !test_locations || !neighbors || !predictions ||
+      !variances)
+    return fail(VGP_E_INVALID, "null pointer");
+  if (m < 1 || m > n_train) return fail(VGP_E_INVALID, "need 1 <= m <= n_train");
+  if (n_test < 0) return fail(VGP_E_INVALID, "negative test count");
+  if (n_test == 0) return VGP_OK;
+  const int64_t np = (int64_t)m + n_test + n_train;
+  if (np > (int64_t)INT32_MAX) return fail(VGP_E_INVALID, "too many points for int32 indices");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  // Point layout [m unused | n_test targets | n_train data]: conditioning
+  // block e (1..n_test) then has its target at m + e - 1, exactly where the
+  // likelihood kernels look, and its neighbours at n_train-relative index +
+  // m + n_test; the per-block mu / sigma_new outputs are the kriging mean and
+  // variance (vg/fit.py:252-264: potrf, two trsv, two dots per test point).
+  Plan* p = new Plan();
+  p->device = device;
+  p->n = np;
+  p->m = m;
+  p->metric = VGP_METRIC_EUCLIDEAN;
+  p->blk_lo = 1;
+  p->blk_hi = n_test + 1;
+  p->rest_lo = 0;
+  p->rest_hi = n_test;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+  p->events = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
+  p->event_pool = new std::vector<cudaEvent_t>();
+  cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return fail(VGP_E_CUDA, cudaGetErrorString(e));
+  }
+  rc = dalloc(&p->d_nbr, (size_t)n_test * m);
+  if (!rc) rc = dalloc(&p->d_pts, np);
+  if (!rc) rc = dalloc(&p->d_rest, n_test);
+  if (!rc) rc = dalloc(&p->d_mu, n_test);
+  if (!rc) rc = dalloc(&p->d_sig, n_test);
+  if (!rc) rc = dalloc(&p->d_fail, 2);
+  const bool fast = dmma_supported(m, cp.kind);
+  if (!rc && !fast && big_needs_scratch(m)) {
+    const int slots = p->num_sms * 2;
+    if (cudaMalloc((void**)&p->d_gscratch, sizeof(double) * (size_t)big_scratch_doubles(m) * slots) ==
+        cudaSuccess)
+      p->gscratch_slots = slots;
+    else
+      rc = fail(VGP_E_NOMEM, "kriging tile scratch");
+  }
+  if (rc) {
+    free_plan(p);
+    return rc;
+  }
+  {
+    std::vector<double4> pts((size_t)np, make_double4(0.0, 0.0, 0.0, 0.0));
+    for (int64_t q = 0; q < n_test; ++q)
+      pts[m + q] = make_double4(test_locations[2 * q], test_locations[2 * q + 1], 0.0, 0.0);
+    for (int64_t i = 0; i < n_train; ++i)
+      pts[m + n_test + i] = make_double4(train_locations[2 * i], train_locations[2 * i + 1],
+                                         train_observations[i], 0.0);
+    std::vector<int32_t> nb((size_t)n_test * m);
+    for (size_t i = 0; i < nb.size(); ++i) {
+      const int64_t v = neighbors[i];
+      if (v < 0 || v >= n_train) {
+        free_plan(p);
+        return fail(VGP_E_INVALID, "neighbour index out of range");
+      }
+      nb[i] = (int32_t)(v + m + n_test);
+    }
+    e = cudaMemcpyAsync(p->d_pts, pts.data(), sizeof(double4) * pts.size(), cudaMemcpyHostToDevice,
+                        p->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->d_nbr, nb.data(), sizeof(int32_t) * nb.size(), cudaMemcpyHostToDevice,
+                          p->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_fail, 0xff, 2 * sizeof(unsigned long long), p->stream);
+    if (e == cudaSuccess)
+      e = fast ? launch_loglik_ws3(*p, cp, 1, n_test + 1, p->stream, false)
+               : launch_loglik_big(*p, cp, 1, n_test + 1, p->stream, false);
+    unsigned long long flags[2] = {0, 0};
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(predictions, p->d_mu, sizeof(double) * n_test, cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(variances, p->d_sig, sizeof(double) * n_test, cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(flags, p->d_fail, sizeof(flags), cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    free_plan(p);
+    if (e != cudaSuccess) return fail(VGP_E_CUDA, std::string("krige: ") + cudaGetErrorString(e));
+    // a non-positive pivot raises like batch_potrf (vg/batchla.py:146-151);
+    // a non-positive variance is returned as is (no check in krige_predict)
+    if (flags[0] != ~0ull) {
+      if (fail_index) *fail_index = npd_key_entry(flags[0], m) - 1;
+      return VGP_NOT_POSITIVE_DEFINITE;
+    }
+  }
+  return VGP_OK;
+}
+
 int vgp_host_register(void* ptr, int64_t bytes) {
   if (!ptr || bytes <= 0) return fail(VGP_E_INVALID, "bad host range");
   VGP_CUDA_TRY(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault));

@@ -172,6 +172,37 @@ def c1_case(with_mle: bool):
     save("c1_n20000_m30_nu05", **out)
 
 
+def krige_cases():
+    """fit.krige_predict (vg/fit.py:221-275) on the reference's own kriging
+    setup (pkg/tests/test_fit.py:82-88) and acceptance criterion 6's split
+    (pkg/tests/test_acceptance.py:150-186, smaller here)."""
+    from vecchiagp import exact, fit
+    from vecchiagp.kernels import KernelParams, KernelSpec
+
+    spec = KernelSpec("matern", KernelParams(1.0, 0.078809, 0.5))
+    rng = np.random.default_rng(200)
+    locs = rng.random((320, 2))
+    y = exact.simulate_grf(locs, spec, seed=201)
+    train, test, truth = locs[:300], locs[300:], y[300:]
+    data = vecchiagp.Dataset(train, y[:300])
+    for m in (1, 25, 40, 90, 300):
+        r = fit.krige_predict(data, spec.params, "matern", test, m, truth)
+        save(f"krige_n300_m{m}_nu05", train=train, y=y[:300], test=test, truth=truth, m=m,
+             family="matern", theta=np.array([1.0, 0.078809, 0.5]),
+             pred=r.predictions, var=r.variances, mse=r.mse)
+    spec2 = KernelSpec("matern", KernelParams(1.3, 0.06, 1.5))
+    rng = np.random.default_rng(700)
+    locs = rng.random((1500, 2))
+    y = exact.simulate_grf(locs, spec2, seed=701)
+    data = vecchiagp.Dataset(locs[:1400], y[:1400])
+    for m, fam, th in ((60, "matern", (1.3, 0.06, 1.5)), (30, "matern", (1.3, 0.06, 0.8)),
+                       (20, "power_exponential", (1.3, 0.06, 1.2))):
+        r = fit.krige_predict(data, KernelParams(*th), fam, locs[1400:], m, y[1400:])
+        save(f"krige_n1400_m{m}_{fam[:6]}", train=locs[:1400], y=y[:1400], test=locs[1400:],
+             truth=y[1400:], m=m, family=fam, theta=np.array(th), pred=r.predictions,
+             var=r.variances, mse=r.mse)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-mle", action="store_true")
@@ -189,6 +220,8 @@ def main():
         knn_cases()
     if args.only in ("", "ll"):
         loglik_cases()
+    if args.only in ("", "krige"):
+        krige_cases()
     if args.only in ("", "c1"):
         c1_case(args.with_mle)
 

@@ -351,3 +351,37 @@ def test_chunked_result_download_vs_oracle(vg, oracle, m, variant):
     np.testing.assert_allclose(res.mu_new, ref.mu_new, rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(res.sigma_new, ref.sigma_new, rtol=1e-5, atol=1e-12)
     assert res.total == plan.device_plan().total(spec)
+
+
+@pytest.mark.parametrize("name", golden_names("krige_"))
+def test_krige_vs_reference_golden(vg, name):
+    """fit.krige_predict on the GPU against the reference's own output
+    (tests/golden/make_golden.py krige_cases): same neighbour sets (bit-exact
+    kNN), predictions to 1e-10 (1e-8 for m = n_train, where the reference
+    switches to its dense path), variances, held-out MSE."""
+    z = load(name)
+    train = vg.Dataset(z["train"], z["y"])
+    s2, beta, nu = (float(v) for v in z["theta"])
+    m = int(z["m"])
+    rep = vg.krige_predict(train, vg.KernelParams(s2, beta, nu), str(z["family"]), z["test"], m,
+                           z["truth"])
+    atol = 1e-8 if m == train.n else 1e-10
+    np.testing.assert_allclose(rep.predictions, z["pred"], rtol=0, atol=atol)
+    np.testing.assert_allclose(rep.variances, z["var"], rtol=1e-7, atol=atol)
+    assert rel(rep.mse, float(z["mse"])) <= 1e-6
+
+
+def test_krige_reference_properties(vg):
+    """pkg/tests/test_fit.py:179-221: a coincident point reproduces its
+    value, a far point shrinks to the mean with the sill as variance,
+    variances are positive and below the sill."""
+    z = load("krige_n300_m40_nu05")
+    train = vg.Dataset(z["train"], z["y"])
+    theta = vg.KernelParams(1.0, 0.078809, 0.5)
+    rep = vg.krige_predict(train, theta, "matern", train.locations[5:6], m=1)
+    assert rep.predictions[0] == pytest.approx(train.observations[5], rel=1e-12)
+    far = vg.krige_predict(train, theta, "matern", np.array([[60.0, 60.0]]), m=30)
+    assert abs(far.predictions[0]) <= 1e-6
+    assert far.variances[0] == pytest.approx(1.0, abs=1e-6)
+    rep = vg.krige_predict(train, theta, "matern", z["test"], m=40)
+    assert np.all(rep.variances > 0.0) and np.all(rep.variances <= 1.0 + 1e-12)

@@ -169,3 +169,42 @@ def test_pin_skips_views_and_small_arrays():
     view = np.zeros((300000, 2))[:, :1]
     V._pin(view)
     assert V._PINNED == before
+
+
+class TestDetrendSqrt:
+    """Restates pkg/tests/test_fit.py:126-175 (host-side data preparation)."""
+
+    def test_plane_removed(self):
+        rng = np.random.default_rng(0)
+        locs = rng.random((40, 2))
+        values = 1.5 - 2.0 * locs[:, 0] + 0.25 * locs[:, 1]
+        res = fit.ols_detrend(geo.Dataset(locs, values))
+        assert np.max(np.abs(res.observations)) <= 1e-10
+
+    def test_residuals_orthogonal_to_design(self):
+        rng = np.random.default_rng(2)
+        locs = rng.random((120, 2))
+        res = fit.ols_detrend(geo.Dataset(locs, rng.standard_normal(120)))
+        design = np.column_stack([np.ones(120), locs[:, 0], locs[:, 1]])
+        assert np.max(np.abs(design.T @ res.observations)) <= 1e-8
+
+    def test_collinear_error(self):
+        locs = np.column_stack([np.arange(5.0), 2.0 * np.arange(5.0)])
+        with pytest.raises(ValueError):
+            fit.ols_detrend(geo.Dataset(locs, np.arange(5.0)))
+
+    def test_sqrt_values_and_negative(self):
+        data = geo.Dataset(np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]]), np.array([4.0, 0.0, 2.25]))
+        np.testing.assert_allclose(fit.sqrt_transform(data).observations, [2.0, 0.0, 1.5], rtol=1e-15)
+        with pytest.raises(ValueError):
+            fit.sqrt_transform(geo.Dataset(np.zeros((1, 2)), np.array([-0.1])))
+
+    def test_krige_validation_before_device(self):
+        data = geo.Dataset(np.random.default_rng(1).random((10, 2)), np.zeros(10))
+        theta = vg.KernelParams(1.0, 0.1, 0.5)
+        with pytest.raises(ValueError):
+            fit.krige_predict(data, theta, "matern", np.zeros((3, 2)), m=0)
+        with pytest.raises(ValueError):
+            fit.krige_predict(data, theta, "matern", np.zeros((3, 2)), m=11)
+        with pytest.raises(ValueError):
+            fit.krige_predict(data, theta, "matern", np.zeros((3, 3)), m=2)
