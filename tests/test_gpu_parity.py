@@ -385,3 +385,45 @@ def test_krige_reference_properties(vg):
     assert far.variances[0] == pytest.approx(1.0, abs=1e-6)
     rep = vg.krige_predict(train, theta, "matern", z["test"], m=40)
     assert np.all(rep.variances > 0.0) and np.all(rep.variances <= 1.0 + 1e-12)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("m,variant", [(30, -1), (60, 7), (90, -1)])
+def test_sharded_partials_bitwise_on_one_gpu(vg, oracle, world, m, variant):
+    """The multi-GPU path with its collective emulated on one device: every
+    rank's shard plan (DevicePlan over shard_blocks' range, its own neighbour
+    rows and distance cache) writes its chunk partials into its slots of the
+    global vector; summing the rank vectors (what the NCCL all-reduce does)
+    and the ordered host sum must reproduce the single-plan total bit for bit
+    — kernels run on block ranges that start mid-table (rest_lo > 0)."""
+    import torch
+
+    from paper_2403_07412_b200.distributed import n_chunks, ordered_total, shard_blocks
+
+    n, seed, beta = 40000, 31, 0.05
+    rng = np.random.default_rng(seed)
+    locs = rng.random((n, 2))
+    data = vg.Dataset(locs, np.zeros(n))
+    plan = vg.make_plan(data, m, "random", seed=seed)
+    y_ord = oracle.simulate_vecchia(locs[plan.permutation.order], m, plan.neighbors.neighbors,
+                                    "matern", 1.0, beta, 1.5, seed + 100)
+    y = np.empty(n)
+    y[plan.permutation.order] = y_ord
+    data = vg.Dataset(locs, y)
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, beta, 1.5))
+    full = vg.vecchia_loglik(data, plan, spec)
+    nvec = 1 + n_chunks(n, m)
+    acc = torch.zeros(nvec, dtype=torch.float64, device="cuda")
+    for r in range(world):
+        lo, hi = shard_blocks(n, m, r, world)
+        if hi <= lo:
+            continue
+        dp = vg.DevicePlan(plan, block_lo=lo, block_hi=hi)
+        dp.set_data(data)
+        dp.set_variant(variant)
+        send = torch.zeros(nvec, dtype=torch.float64, device="cuda")
+        dp.partials_device(spec, send.data_ptr())
+        torch.cuda.synchronize()
+        acc += send
+        dp.close()
+    assert ordered_total(acc.cpu().numpy()) == full.total
