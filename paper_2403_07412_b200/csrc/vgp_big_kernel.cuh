@@ -47,7 +47,7 @@ using ws::tidx;
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kGroup = 4;  // tiles per warp in flight
-constexpr int kHead = 256 + 64 + 8;  // exp table | Lt | Iv
+constexpr int kHead = 256 + 64 + 8 + 5 * kBesselTab;  // exp table | Lt | Iv | Bessel tables
 
 __host__ __device__ inline int ntiles_of(int m) { return (m + 2 + 7) / 8; }
 // doubles of the shared-memory area besides the tiles
@@ -62,9 +62,16 @@ __host__ __device__ inline int64_t tile_doubles(int m) {
 // vg/kernels.py:59-91) with C(0) = sigma^2 exactly (d below 1e-100: the
 // diagonal and exact duplicates, whose distance is 2^-500 by construction)
 template <int KIND>
-__device__ __forceinline__ double cov_any(double d, const CovParams& cp, const double* tab) {
+__device__ __forceinline__ double cov_any(double d, const CovParams& cp, const double* tab,
+                                          const double* btab) {
   if (KIND <= kMatern25) return cov_lean<KIND>(d, cp.inv_beta, tab);
-  return d < 1e-100 ? cp.s2 : cov_ref(cp, d);
+  if (d < 1e-100) return cp.s2;
+  if (KIND == kMaternGen) {
+    // s2 2^(1-nu)/Gamma(nu) u^nu K_nu(u), u = d / beta (vg/kernels.py:75-81)
+    const double u = d / cp.beta;
+    return cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k_tab(cp, u, btab);
+  }
+  return cov_ref(cp, d);
 }
 
 template <int KIND, bool CACHE, bool GT>
@@ -82,6 +89,7 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   double* tabw = smem;
   double* Lt = smem + 256;  // L_cc transposed: Lt[8k + j] = L[j][k]
   double* Iv = Lt + 64;     // reciprocal pivots
+  double* Bt = Iv + 8;      // general-nu Bessel reciprocal tables
   double* O = smem + kHead;  // yJ row (row m+1)
   double2* XY = reinterpret_cast<double2*>(O + P);
   double* Y = O + 3 * P;  // target observation
@@ -92,6 +100,7 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   const int q = lane & 3;   // fragment column pair
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tabw[i] = s2 * kExp2Table[i];
+  if (KIND == kMaternGen) bessel_fill_tab(cp, Bt, threadIdx.x, blockDim.x);
   __syncthreads();
   const double* tab = smem;
   auto tile = [&](int I, int J) -> double* { return T + (size_t)tidx(I, J) * 64; };
@@ -125,16 +134,16 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             double v0, v1;
             if (CACHE) {
               const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, c) * 64 + chunk_off(r, q)));
-              v0 = cov_any<KIND>(dv.x, cp, tab);
-              v1 = cov_any<KIND>(dv.y, cp, tab);
+              v0 = cov_any<KIND>(dv.x, cp, tab, Bt);
+              v1 = cov_any<KIND>(dv.y, cp, tab, Bt);
             } else {
               const double2 pa = XY[i < P ? i : 0];
               const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * c + 2 * q);
               double dx = pa.x - pb.x, dy = pa.y - pb.y;
-              v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab);
+              v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
               dx = pa.x - pb.z;
               dy = pa.y - pb.w;
-              v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab);
+              v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
             }
             if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
               const double2 ov = ld2(O + 8 * c + 2 * q);
