@@ -42,6 +42,7 @@ using ll::mma;
 using ll::rsqrt_chain;
 using ll::st2;
 using ws::chunk_off;
+using ws::ntri;
 using ws::tidx;
 
 constexpr int kWarps = 4;
@@ -54,7 +55,7 @@ __host__ __device__ inline int ntiles_of(int m) { return (m + 2 + 7) / 8; }
 __host__ __device__ inline int head_doubles(int m) { return kHead + 3 * 8 * ntiles_of(m) + 4; }
 __host__ __device__ inline int64_t tile_doubles(int m) {
   const int nt = ntiles_of(m);
-  return (int64_t)tidx(nt, 0) * 64;
+  return (int64_t)ntri(nt) * 64;
 }
 
 // covariance at distance d: lean closed forms, or the reference expression
@@ -103,7 +104,7 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   if (KIND == kMaternGen) bessel_fill_tab(cp, Bt, threadIdx.x, blockDim.x);
   __syncthreads();
   const double* tab = smem;
-  auto tile = [&](int I, int J) -> double* { return T + (size_t)tidx(I, J) * 64; };
+  auto tile = [&](int I, int J) -> double* { return T + (size_t)tidx(I, J, NT) * 64; };
 
   int fj = -1;  // warp 0: first non-positive pivot column of the current block
   for (int64_t e = e_lo + blockIdx.x; e < e_hi; e += gridDim.x) {
@@ -133,7 +134,7 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             const int i = 8 * I + r;
             double v0, v1;
             if (CACHE) {
-              const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, c) * 64 + chunk_off(r, q)));
+              const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, c, NT) * 64 + chunk_off(r, q)));
               v0 = cov_any<KIND>(dv.x, cp, tab, Bt);
               v1 = cov_any<KIND>(dv.y, cp, tab, Bt);
             } else {

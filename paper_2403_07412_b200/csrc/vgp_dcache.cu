@@ -34,12 +34,12 @@ build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__
     // tile (I, J), J <= I < NT, row r, column col: d(8I + r, 8J + col) on and
     // below the diagonal for rows <= m, else 0; ws::chunk_off swizzle
     const int nt = (m + 2 + 7) / 8;
-    const int total = ws::tidx(nt, 0) * 64;
+    const int total = ws::ntri(nt) * 64;
     for (int idx = lane; idx < total; idx += 32) {
       const int t = idx >> 6, w = idx & 63;
-      int I = 0;
-      while (ws::tidx(I + 1, 0) <= t) ++I;
-      const int J = t - ws::tidx(I, 0);
+      int J = 0, tt = t;
+      while (tt >= nt - J) tt -= nt - J++;
+      const int I = J + tt;
       const int rr = w >> 3, col = w & 7;
       const int i = 8 * I + rr, k = 8 * J + col;
       double d = 0.0;
@@ -63,7 +63,7 @@ __global__ void diff_kernel(const double* __restrict__ a, const double* __restri
 
 }  // namespace
 
-int64_t dcache_stride(int m) { return (int64_t)ws::tidx((m + 2 + 7) / 8, 0) * 64; }
+int64_t dcache_stride(int m) { return (int64_t)ws::ntri((m + 2 + 7) / 8) * 64; }
 
 cudaError_t launch_build_dcache(const Plan& p, cudaStream_t stream) {
   const int64_t e_lo = p.rest_lo + 1, e_hi = p.rest_hi + 1;

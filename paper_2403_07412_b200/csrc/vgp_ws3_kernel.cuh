@@ -30,7 +30,7 @@
 // column.  8 blocks in flight per SM (8 x 20.8 KB of shared memory).
 //
 // Shared memory per block: the tile triangle (tile (I, J) at
-// (I (I+1)/2 + J) * 64 doubles, ws::chunk_off swizzle: conflict-free fragment
+// (J NT - J (J-1)/2 + I - J) * 64 doubles, column-major, ws::chunk_off swizzle: conflict-free fragment
 // and row accesses), staging S for the last panel (the tile triangle is then
 // refilled with the next block's distances by one cp.async.bulk + mbarrier),
 // the yJ row, coordinates (uncached variant) and the target observation.
@@ -54,6 +54,7 @@ using ll::st2;
 using ws::bar_arrive;
 using ws::bar_sync;
 using ws::chunk_off;
+using ws::ntri;
 using ws::tidx;
 
 constexpr int kSlots = 8;    // blocks in flight per CTA (= per SM)
@@ -68,7 +69,7 @@ struct SlotLayout {
   int stride;  // tiles | S (2 tiles) | O (P) | XY (2P) | yt (2) | mbarrier (2)
 };
 __host__ __device__ constexpr SlotLayout slot_layout(int nt) {
-  return SlotLayout{tidx(nt, 0) * 64, tidx(nt, 0) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2};
+  return SlotLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2};
 }
 
 template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false>
@@ -200,7 +201,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                 const int i = 8 * I + r;
                 double v0, v1;
                 if (CACHE) {
-                  const double2 dv = ld2(T + tidx(I, c) * 64 + chunk_off(r, q));
+                  const double2 dv = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
                   v0 = cov_lean<KIND>(dv.x, inv_beta, tab);
                   v1 = cov_lean<KIND>(dv.y, inv_beta, tab);
                 } else {
@@ -224,11 +225,11 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             }
             // ---- left-looking update with L of tile columns k < c
             auto update = [&](const int k) {
-              const double2 b = ld2(T + tidx(c, k) * 64 + chunk_off(r, q));
+              const double2 b = ld2(T + tidx(c, k, NT) * 64 + chunk_off(r, q));
               double2 a[NT];
 #pragma unroll
               for (int I = 0; I < NT; ++I)
-                if (I > c) a[I] = ld2(T + tidx(I, k) * 64 + chunk_off(r, q));
+                if (I > c) a[I] = ld2(T + tidx(I, k, NT) * 64 + chunk_off(r, q));
               a[c] = b;
               if (k == c - 1) mark(s, 1, 3 + 2 * c);
 #pragma unroll
@@ -260,7 +261,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
 #pragma unroll
             for (int I = 0; I < NT; ++I) {
               if (I >= c) {
-                double* dst = lastc ? Sb(s) + (I - c) * 64 : T + tidx(I, c) * 64;
+                double* dst = lastc ? Sb(s) + (I - c) * 64 : T + tidx(I, c, NT) * 64;
                 st2(dst + chunk_off(r, q), acc[I][0], acc[I][1]);
               }
             }
@@ -291,7 +292,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
           double a[kMaxRows][8];
           auto row_ptr = [&](int rr) -> double* {
             const int I = c + ((lane + 32 * rr) >> 3);
-            return lastc ? S + (I - c) * 64 : T + tidx(I < NT ? I : NT - 1, c) * 64;
+            return lastc ? S + (I - c) * 64 : T + tidx(I < NT ? I : NT - 1, c, NT) * 64;
           };
 #pragma unroll
           for (int rr = 0; rr < kMaxRows; ++rr) {

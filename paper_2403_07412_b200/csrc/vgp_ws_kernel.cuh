@@ -23,7 +23,7 @@
 // next column run underneath it instead of after it.
 //
 // Shared memory per pair: the lower tile triangle, tile (I, J) at
-// (I (I+1)/2 + J) * 64 doubles; row r of a tile is 4 16-byte chunks, chunk x
+// (J NT - J (J-1)/2 + I - J) * 64 doubles, column-major; row r of a tile is 4 16-byte chunks, chunk x
 // stored at position x ^ ((r >> 1) & 3), so both the DMMA fragment accesses
 // (lane (r, q) -> chunk q of row r) and the panel's row accesses (lane -> one
 // row, all chunks) are bank-conflict free.  A tile holds, in turn, the
@@ -60,7 +60,11 @@ constexpr int kPairs = 4;              // blocks in flight per CTA
 constexpr int kThreads = 64 * kPairs;  // warps 0..kPairs-1 chain, kPairs..2kPairs-1 worker
 constexpr int kHead = 256;             // sigma^2-scaled exp table
 
-__host__ __device__ constexpr int tidx(int I, int J) { return I * (I + 1) / 2 + J; }
+// tiles of the lower tile triangle, column-major: tile column J is a
+// contiguous run of nt - J tiles (column 0 first, so a block's first
+// column can be streamed ahead of the rest)
+__host__ __device__ constexpr int ntri(int nt) { return nt * (nt + 1) / 2; }
+__host__ __device__ constexpr int tidx(int I, int J, int nt) { return J * nt - J * (J - 1) / 2 + (I - J); }
 // doubles offset of 16-byte chunk x (columns 2x, 2x+1 or x, x+4) of row r in a tile
 __host__ __device__ constexpr int chunk_off(int r, int x) { return 8 * r + 2 * (x ^ ((r >> 1) & 3)); }
 
@@ -69,7 +73,7 @@ struct PairLayout {
   int stride;  // doubles per pair: tiles | S (2 tiles) | O (P) | XY (2P) | yt (4) | mbarrier (2)
 };
 __host__ __device__ constexpr PairLayout pair_layout(int nt) {
-  return PairLayout{tidx(nt, 0) * 64, tidx(nt, 0) * 64 + 128 + 8 * nt + 16 * nt + 4 + 2};
+  return PairLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 4 + 2};
 }
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
@@ -204,7 +208,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
               const int i = 8 * I + r;
               double v0, v1;
               if (CACHE) {
-                const double2 dv = ld2(T + tidx(I, c) * 64 + chunk_off(r, q));
+                const double2 dv = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
                 v0 = cov_lean<KIND>(dv.x, inv_beta, tab);
                 v1 = cov_lean<KIND>(dv.y, inv_beta, tab);
               } else {
@@ -227,11 +231,11 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
           }
           // ---- left-looking update with L of tile columns k < c
           auto update = [&](const int k) {
-            const double2 b = ld2(T + tidx(c, k) * 64 + chunk_off(r, q));
+            const double2 b = ld2(T + tidx(c, k, NT) * 64 + chunk_off(r, q));
             double2 a[NT];
 #pragma unroll
             for (int I = 0; I < NT; ++I)
-              if (I > c) a[I] = ld2(T + tidx(I, k) * 64 + chunk_off(r, q));
+              if (I > c) a[I] = ld2(T + tidx(I, k, NT) * 64 + chunk_off(r, q));
             a[c] = b;
             if (k == c - 1) mark(3 + 2 * c);
 #pragma unroll
@@ -264,7 +268,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
 #pragma unroll
           for (int I = 0; I < NT; ++I) {
             if (I >= c) {
-              double* dst = lastc ? S + (I - c) * 64 : T + tidx(I, c) * 64;
+              double* dst = lastc ? S + (I - c) * 64 : T + tidx(I, c, NT) * 64;
               st2(dst + chunk_off(r, q), acc[I][0], acc[I][1]);
             }
           }
@@ -292,7 +296,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
           double a[kMaxRows][8];
           auto row_ptr = [&](int rr) -> double* {
             const int I = c + ((lane + 32 * rr) >> 3);
-            return lastc ? S + (I - c) * 64 : T + tidx(I, c) * 64;
+            return lastc ? S + (I - c) * 64 : T + tidx(I, c, NT) * 64;
           };
 #pragma unroll
           for (int rr = 0; rr < kMaxRows; ++rr) {
