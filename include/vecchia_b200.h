@@ -70,6 +70,16 @@ int vgp_device_count(int* count);
 int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t m,
                          int64_t* neighbors);
 
+/* Great-circle kNN — replaces numba geo._topm_sphere (vg/geo.py:266-292) as
+ * called by nearest_neighbors (predecessors != 0: queries are data[m..nd),
+ * candidates j < target) and nearest_points (predecessors == 0: queries
+ * query3, every candidate).  Points are rows (lambda, phi, cos phi) in
+ * radians, computed by the caller exactly as the reference does (numpy
+ * radians / cos, vg/geo.py:305-310); the per-pair key is the haversine of
+ * the central angle.  Exact up to keys tied within CUDA's 1-ulp sin. */
+int vgp_knn_sphere(int device, const double* data3, int64_t nd, const double* query3, int64_t nq,
+                   int32_t m, int predecessors, int64_t* neighbors);
+
 /* Replaces geo.nearest_points (vg/geo.py:350-358): unrestricted m nearest
  * data points per query row (kriging). neighbors: (nq, m) int64. */
 int vgp_knn_points(int device, const double* query, int64_t nq, const double* data, int64_t nd,
@@ -115,12 +125,14 @@ int vgp_plan_set_data(vgp_plan* plan, const double* locations, const double* obs
  * neighbors: n_test x m training indices (geo.nearest_points, e.g. from
  * vgp_knn_points).  Writes the conditional means (predictions) and variances
  * sigma^2 - v'v'.  Returns VGP_NOT_POSITIVE_DEFINITE with *fail_index = the
- * test point whose conditioning matrix has a non-positive pivot.  Euclidean
- * metric. */
+ * test point whose conditioning matrix has a non-positive pivot.  metric:
+ * VGP_METRIC_EUCLIDEAN or VGP_METRIC_GREAT_CIRCLE (degrees, radius in the
+ * distance unit). */
 int vgp_krige(int device, const double* train_locations, const double* train_observations,
               int64_t n_train, const double* test_locations, int64_t n_test, int32_t m,
-              const int64_t* neighbors, int family, double sigma_sq, double beta, double nu,
-              double* predictions, double* variances, int64_t* fail_index);
+              const int64_t* neighbors, int metric, double radius, int family, double sigma_sq,
+              double beta, double nu, double* predictions, double* variances,
+              int64_t* fail_index);
 
 /* Page-lock a host range so uploads from it (vgp_plan_set_data) and result
  * downloads into it run as asynchronous DMA (cudaHostRegister); the Python

@@ -196,14 +196,34 @@ def is_closed_form(family: str, nu: float) -> bool:
     return family == "power_exponential" or nu in (0.5, 1.5, 2.5)
 
 
+def _haversine(lon1, lat1, lon2, lat2, radius):
+    # vg/geo.py:70-79, the same numpy expression
+    p1 = np.radians(lat1)
+    p2 = np.radians(lat2)
+    l1 = np.radians(lon1)
+    l2 = np.radians(lon2)
+    h = np.sin((p2 - p1) / 2.0) ** 2 + np.cos(p1) * np.cos(p2) * np.sin((l2 - l1) / 2.0) ** 2
+    return 2.0 * radius * np.arcsin(np.sqrt(np.clip(h, 0.0, 1.0)))
+
+
+def _pdist(a, b, metric, radius):
+    """geo.pairwise_distance (vg/geo.py:92-98) on broadcast (..., 2) arrays."""
+    if metric == "great_circle":
+        return _haversine(a[..., 0], a[..., 1], b[..., 0], b[..., 1], radius)
+    return np.hypot(a[..., 0] - b[..., 0], a[..., 1] - b[..., 1])
+
+
 def loglik(ordered_locs, ordered_obs, m: int, neighbors, family: str, sigma_sq: float,
-           beta: float, nu: float, threads: int | None = None) -> OracleResult:
+           beta: float, nu: float, threads: int | None = None, metric: str = "euclidean",
+           radius: float = 6371.0) -> OracleResult:
     """Vecchia log-likelihood of an ORDERED dataset (vg/vecchia.py:217-238).
 
-    Closed-form kernels run in the C restatement; general nu in numpy+scipy.
+    Closed-form kernels on the plane run in the C restatement; general nu and
+    the great-circle metric in numpy+scipy.
     """
-    if not is_closed_form(family, nu):
-        return loglik_numpy(ordered_locs, ordered_obs, m, neighbors, family, sigma_sq, beta, nu)
+    if not is_closed_form(family, nu) or metric != "euclidean":
+        return loglik_numpy(ordered_locs, ordered_obs, m, neighbors, family, sigma_sq, beta, nu,
+                            metric=metric, radius=radius)
     locs = np.ascontiguousarray(ordered_locs, dtype=np.float64)
     obs = np.ascontiguousarray(ordered_obs, dtype=np.float64)
     nbr = np.ascontiguousarray(neighbors, dtype=np.int64)
@@ -258,7 +278,8 @@ def _dot(a, b):
 
 
 def loglik_numpy(ordered_locs, ordered_obs, m, neighbors, family, sigma_sq, beta, nu,
-                 chunk: int | None = None) -> OracleResult:
+                 chunk: int | None = None, metric: str = "euclidean",
+                 radius: float = 6371.0) -> OracleResult:
     """Vectorised numpy restatement of assemble/_numeric_stage/_reduction_stage."""
     locs = np.asarray(ordered_locs, dtype=np.float64)
     y = np.asarray(ordered_obs, dtype=np.float64)
@@ -268,15 +289,15 @@ def loglik_numpy(ordered_locs, ordered_obs, m, neighbors, family, sigma_sq, beta
     mats = np.empty((count, m, m))
     vv = np.empty((count, m))
     yv = np.empty((count, m))
-    d0 = np.hypot(locs[:m, None, 0] - locs[None, :m, 0], locs[:m, None, 1] - locs[None, :m, 1])
+    d0 = _pdist(locs[:m, None, :], locs[None, :m, :], metric, radius)
     mats[0] = cov(d0, family, sigma_sq, beta, nu)
     vv[0] = y[:m]
     yv[0] = y[:m]
     if count > 1:
         nl = locs[nbr]  # (count-1, m, 2)
-        dm = np.hypot(nl[:, :, None, 0] - nl[:, None, :, 0], nl[:, :, None, 1] - nl[:, None, :, 1])
+        dm = _pdist(nl[:, :, None, :], nl[:, None, :, :], metric, radius)
         mats[1:] = cov(dm, family, sigma_sq, beta, nu)
-        dv = np.hypot(locs[m:, None, 0] - nl[:, :, 0], locs[m:, None, 1] - nl[:, :, 1])
+        dv = _pdist(locs[m:, None, :], nl, metric, radius)
         vv[1:] = cov(dv, family, sigma_sq, beta, nu)
         yv[1:] = y[nbr]
     # column-major semantics do not matter for symmetric input; work on (k, i, j)

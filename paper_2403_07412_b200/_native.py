@@ -41,7 +41,7 @@ EXPORTS = (
     "vgp_knn_points", "vgp_cov", "vgp_bessel_kv", "vgp_plan_create", "vgp_plan_set_data",
     "vgp_plan_destroy", "vgp_loglik", "vgp_loglik_partials", "vgp_plan_info",
     "vgp_plan_set_variant", "vgp_plan_stream", "vgp_loglik_async", "vgp_plan_fetch",
-    "vgp_host_register", "vgp_host_unregister", "vgp_krige",
+    "vgp_host_register", "vgp_host_unregister", "vgp_krige", "vgp_knn_sphere",
     "vgp_batch_potrf", "vgp_batch_trsv", "vgp_batch_dot", "vgp_loglik_partials_device",
     "vgp_plan_set_timing", "vgp_plan_kernel_time",
 )
@@ -90,7 +90,9 @@ _sig("vgp_plan_create", _int, [_int, _i64, _i32, _int, _d, _ip, _ip, _i64, _i64,
                                ctypes.POINTER(_vp)])
 _sig("vgp_plan_set_data", _int, [_vp, _dp, _dp])
 _sig("vgp_host_register", _int, [_vp, _i64])
-_sig("vgp_krige", _int, [_int, _dp, _dp, _i64, _dp, _i64, _i32, _ip, _int, _d, _d, _d, _dp, _dp, _ip])
+_sig("vgp_knn_sphere", _int, [_int, _dp, _i64, _dp, _i64, _i32, _int, _ip])
+_sig("vgp_krige", _int, [_int, _dp, _dp, _i64, _dp, _i64, _i32, _ip, _int, _d, _int, _d, _d, _d,
+                         _dp, _dp, _ip])
 _sig("vgp_host_unregister", _int, [_vp])
 _sig("vgp_plan_destroy", _int, [_vp])
 _sig("vgp_loglik", _int, [_vp, _int, _d, _d, _d, _dp, _ip, _dp, _dp, _dp, _dp])

@@ -220,18 +220,21 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     // (5, 6, 9, 10: retired experiments),
     // 7 scheduler-aware warp-specialised, 8 the same + distance cache,
     // 11 large-m CTA-per-block, 12 the same + distance cache
-    const bool fast = dmma_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN;
-    const bool large = !fast && big_supported(p->m, cp.kind) && p->metric == VGP_METRIC_EUCLIDEAN &&
-                       (!big_needs_scratch(p->m) || p->d_gscratch);
+    // The DMMA kernels only need distances: with the distance cache (built
+    // for either metric) they cover great-circle plans too; computing
+    // distances on the fly they are Euclidean only.
+    const bool eu = p->metric == VGP_METRIC_EUCLIDEAN;
     const bool cached = p->d_dcache && p->dcache_valid;
+    const bool fast_c = dmma_supported(p->m, cp.kind) && cached;
+    const bool fast_n = dmma_supported(p->m, cp.kind) && eu;
+    const bool scratch_ok = !big_needs_scratch(p->m) || p->d_gscratch;
+    const bool big_c = big_supported(p->m, cp.kind) && cached && scratch_ok;
+    const bool big_n = big_supported(p->m, cp.kind) && eu && scratch_ok;
     int v = p->force_variant;
-    if (v < 0) v = fast ? (cached ? 8 : 7) : (large ? (cached ? 12 : 11) : 0);
-    if (v > 0 && v <= 10 && !fast)
-      return fail(VGP_E_UNSUPPORTED, "warp-DMMA variants do not cover this m / kernel");
-    if (v >= 11 && !(fast || large))
-      return fail(VGP_E_UNSUPPORTED, "large-m DMMA variant does not cover this m / kernel");
-    if ((v == 4 || v == 6 || v == 8 || v == 10 || v == 12) && !cached)
-      return fail(VGP_E_UNSUPPORTED, "no distance cache on this plan");
+    if (v < 0) v = fast_c ? 8 : (fast_n ? 7 : (big_c ? 12 : (big_n ? 11 : 0)));
+    const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
+                    ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c);
+    if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
       int rc = take_event(p, &ev0);
@@ -350,6 +353,60 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn: ") + cudaGetErrorString(e));
   cudaFree(d_pts);
+  cudaFree(d_out);
+  cudaFree(d_keys);
+  cudaFree(d_idx);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+int vgp_knn_sphere(int device, const double* data3, int64_t nd, const double* query3, int64_t nq,
+                   int32_t m, int predecessors, int64_t* neighbors) {
+  if (!data3 || !neighbors || (!predecessors && !query3)) return fail(VGP_E_INVALID, "null pointer");
+  if (predecessors) {
+    if (m < 1 || nd <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
+    nq = nd - m;
+  } else if (m < 1 || m > nd) {
+    return fail(VGP_E_INVALID, "need 1 <= m <= nd");
+  }
+  if (nd > (int64_t)INT32_MAX) return fail(VGP_E_INVALID, "n exceeds int32 index range");
+  if (nq <= 0) return VGP_OK;
+  int rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  std::vector<double4> hd((size_t)nd), hq(predecessors ? 0 : (size_t)nq);
+  for (int64_t i = 0; i < nd; ++i) hd[i] = make_double4(data3[3 * i], data3[3 * i + 1], data3[3 * i + 2], 0.0);
+  for (int64_t i = 0; i < (int64_t)hq.size(); ++i)
+    hq[i] = make_double4(query3[3 * i], query3[3 * i + 1], query3[3 * i + 2], 0.0);
+  cudaStream_t s;
+  VGP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double4 *d_data = nullptr, *d_q = nullptr;
+  int64_t* d_out = nullptr;
+  double* d_keys = nullptr;
+  int32_t* d_idx = nullptr;
+  const int64_t batch = std::min<int64_t>(nq, int64_t(1) << 20);
+  const int64_t slots = ((batch + 127) / 128) * 128;
+  rc = dalloc(&d_data, nd);
+  if (!rc && !predecessors) rc = dalloc(&d_q, nq);
+  if (!rc) rc = dalloc(&d_out, (size_t)batch * m);
+  if (!rc) rc = dalloc(&d_keys, (size_t)slots * m);
+  if (!rc) rc = dalloc(&d_idx, (size_t)slots * m);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpyAsync(d_data, hd.data(), sizeof(double4) * nd, cudaMemcpyHostToDevice, s);
+  if (!rc && e == cudaSuccess && !predecessors)
+    e = cudaMemcpyAsync(d_q, hq.data(), sizeof(double4) * nq, cudaMemcpyHostToDevice, s);
+  for (int64_t q0 = 0; !rc && e == cudaSuccess && q0 < nq; q0 += batch) {
+    int64_t qn = std::min(batch, nq - q0);
+    e = predecessors ? launch_knn_sphere(d_data, nd, d_data + m + q0, qn, q0, 1, m, d_out, d_keys, d_idx, s)
+                     : launch_knn_sphere(d_data, nd, d_q + q0, qn, q0, 0, m, d_out, d_keys, d_idx, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(neighbors + q0 * m, d_out, sizeof(int64_t) * qn * m,
+                          cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn sphere: ") + cudaGetErrorString(e));
+  cudaFree(d_data);
+  cudaFree(d_q);
   cudaFree(d_out);
   cudaFree(d_keys);
   cudaFree(d_idx);
@@ -519,7 +576,7 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
       rc = dalloc(&p->d_work, p->work_doubles);
     }
   }
-  if (!rc && nrest > 0 && big_supported(m, kMatern15) && metric == VGP_METRIC_EUCLIDEAN) {
+  if (!rc && nrest > 0 && big_supported(m, kMatern15)) {
     // distance cache: on unless VGP_DCACHE=0, and only when it fits in half
     // of the free device memory
     const char* env = std::getenv("VGP_DCACHE");
@@ -592,14 +649,17 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
 
 int vgp_krige(int device, const double* train_locations, const double* train_observations,
               int64_t n_train, const double* test_locations, int64_t n_test, int32_t m,
-              const int64_t* neighbors, int family, double sigma_sq, double beta, double nu,
-              double* predictions, double* variances, int64_t* fail_index) {
+              const int64_t* neighbors, int metric, double radius, int family, double sigma_sq,
+              double beta, double nu, double* predictions, double* variances,
+              int64_t* fail_index) {
   if (fail_index) *fail_index = -1;
   if (!train_locations || !train_observations || !test_locations || !neighbors || !predictions ||
       !variances)
     return fail(VGP_E_INVALID, "null pointer");
   if (m < 1 || m > n_train) return fail(VGP_E_INVALID, "need 1 <= m <= n_train");
   if (n_test < 0) return fail(VGP_E_INVALID, "negative test count");
+  if (metric != VGP_METRIC_EUCLIDEAN && metric != VGP_METRIC_GREAT_CIRCLE)
+    return fail(VGP_E_INVALID, "unknown metric");
   if (n_test == 0) return VGP_OK;
   const int64_t np = (int64_t)m + n_test + n_train;
   if (np > (int64_t)INT32_MAX) return fail(VGP_E_INVALID, "too many points for int32 indices");
@@ -618,7 +678,8 @@ int vgp_krige(int device, const double* train_locations, const double* train_obs
   p->device = device;
   p->n = np;
   p->m = m;
-  p->metric = VGP_METRIC_EUCLIDEAN;
+  p->metric = metric;
+  p->radius = radius;
   p->blk_lo = 1;
   p->blk_hi = n_test + 1;
   p->rest_lo = 0;
@@ -638,6 +699,13 @@ int vgp_krige(int device, const double* train_locations, const double* train_obs
   if (!rc) rc = dalloc(&p->d_sig, n_test);
   if (!rc) rc = dalloc(&p->d_fail, 2);
   const bool fast = dmma_supported(m, cp.kind);
+  // great-circle: the kernels take haversine distances from a one-shot
+  // distance cache (vgp_dcache.cu); Euclidean distances are computed in place
+  const bool gcd = metric == VGP_METRIC_GREAT_CIRCLE;
+  if (!rc && gcd) {
+    p->dcache_stride = dcache_stride(m);
+    rc = dalloc(&p->d_dcache, (size_t)p->dcache_stride * n_test);
+  }
   if (!rc && !fast && big_needs_scratch(m)) {
     const int slots = p->num_sms * 2;
     if (cudaMalloc((void**)&p->d_gscratch, sizeof(double) * (size_t)big_scratch_doubles(m) * slots) ==
@@ -672,9 +740,13 @@ int vgp_krige(int device, const double* train_locations, const double* train_obs
       e = cudaMemcpyAsync(p->d_nbr, nb.data(), sizeof(int32_t) * nb.size(), cudaMemcpyHostToDevice,
                           p->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->d_fail, 0xff, 2 * sizeof(unsigned long long), p->stream);
+    if (e == cudaSuccess && gcd) {
+      e = launch_build_dcache(*p, p->stream);
+      p->dcache_valid = e == cudaSuccess;
+    }
     if (e == cudaSuccess)
-      e = fast ? launch_loglik_ws3(*p, cp, 1, n_test + 1, p->stream, false)
-               : launch_loglik_big(*p, cp, 1, n_test + 1, p->stream, false);
+      e = fast ? launch_loglik_ws3(*p, cp, 1, n_test + 1, p->stream, gcd)
+               : launch_loglik_big(*p, cp, 1, n_test + 1, p->stream, gcd);
     unsigned long long flags[2] = {0, 0};
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(predictions, p->d_mu, sizeof(double) * n_test, cudaMemcpyDeviceToHost, p->stream);

@@ -8,6 +8,7 @@
 // of vgp_ws_kernel.cuh (same formula), so cached and uncached evaluations
 // agree bit for bit.
 #include "vgp_internal.cuh"
+#include "vgp_math.cuh"
 #include "vgp_ws_kernel.cuh"
 
 namespace vgp {
@@ -18,7 +19,7 @@ constexpr int kWarps = 4;
 __global__ void __launch_bounds__(kWarps * 32)
 build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
                     int64_t e_lo, int64_t e_hi, int64_t rest_lo, double* __restrict__ cache,
-                    int64_t cstride) {
+                    int64_t cstride, int metric, double radius) {
   extern __shared__ double2 sxy[];  // kWarps x (m + 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* XY = sxy + warp * (m + 1);
@@ -44,9 +45,14 @@ build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__
       const int i = 8 * I + rr, k = 8 * J + col;
       double d = 0.0;
       if (k <= i && i <= m) {
-        const double dx = XY[i].x - XY[k].x;
-        const double dy = XY[i].y - XY[k].y;
-        d = sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000)));  // as vgp_ws_kernel.cuh
+        if (metric == VGP_METRIC_GREAT_CIRCLE) {
+          // haversine, vg/geo.py:70-79 (degrees; 0 for coincident points)
+          d = dist_gcd(XY[k].x, XY[k].y, XY[i].x, XY[i].y, radius);
+        } else {
+          const double dx = XY[i].x - XY[k].x;
+          const double dy = XY[i].y - XY[k].y;
+          d = sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000)));  // as vgp_ws_kernel.cuh
+        }
       }
       out[t * 64 + ws::chunk_off(rr, col >> 1) + (col & 1)] = d;
     }
@@ -72,7 +78,7 @@ cudaError_t launch_build_dcache(const Plan& p, cudaStream_t stream) {
   const int grid = (int)(want < (int64_t)p.num_sms * 8 ? want : (int64_t)p.num_sms * 8);
   const size_t sm = sizeof(double2) * kWarps * (p.m + 1);
   build_dcache_kernel<<<grid, kWarps * 32, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi,
-                                                          p.rest_lo, p.d_dcache, p.dcache_stride);
+                                                          p.rest_lo, p.d_dcache, p.dcache_stride, p.metric, p.radius);
   return cudaGetLastError();
 }
 

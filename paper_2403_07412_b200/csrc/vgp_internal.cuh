@@ -108,6 +108,11 @@ cudaError_t launch_knn(const double2* d_data, int64_t nd, const double2* d_query
                        int64_t q_offset, int pred, int32_t m, int64_t* d_out, double* d_keys,
                        int32_t* d_idx, cudaStream_t stream);
 
+// Sphere kNN (vg/geo.py:266-292); points (lambda, phi, cos phi, 0) in radians.
+cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* d_query, int64_t nq,
+                              int64_t q_offset, int pred, int32_t m, int64_t* d_out, double* d_keys,
+                              int32_t* d_idx, cudaStream_t stream);
+
 // Permute raw (x, y, obs) rows into ordered double4 points.
 cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t n,
                            double4* d_pts, cudaStream_t stream);

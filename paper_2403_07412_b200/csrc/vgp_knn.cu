@@ -16,29 +16,42 @@ namespace {
 constexpr int kKnnThreads = 128;
 constexpr int kKnnTile = 1024;  // candidates per shared-memory tile (16 KiB)
 
-__device__ __forceinline__ double knn_key(double xj, double yj, double xt, double yt) {
-  double dx = __dsub_rn(xj, xt);
-  double dy = __dsub_rn(yj, yt);
+__device__ __forceinline__ double knn_key(double2 c, double2 t) {
+  double dx = __dsub_rn(c.x, t.x);
+  double dy = __dsub_rn(c.y, t.y);
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+}
+
+// geo._topm_sphere (vg/geo.py:266-292): points are (lambda, phi, cos phi) in
+// radians, computed on the host with numpy exactly as the reference's
+// _topm_scan does (vg/geo.py:305-310); key = haversine of the central angle
+//   sp * sp + ((cos_t * cos_j) * sl) * sl,  sp = sin((phi_j - phi_t) / 2),
+//   sl = sin((lambda_j - lambda_t) / 2), every op rounded separately.
+// CUDA's sin is within 1 ulp of glibc's (the reference's numba calls libm),
+// so sphere neighbour sets are exact except for keys tied to the last ulp.
+__device__ __forceinline__ double knn_key(double4 c, double4 t) {
+  const double sp = sin(__dmul_rn(__dsub_rn(c.y, t.y), 0.5));
+  const double sl = sin(__dmul_rn(__dsub_rn(c.x, t.x), 0.5));
+  return __dadd_rn(__dmul_rn(sp, sp), __dmul_rn(__dmul_rn(__dmul_rn(t.z, c.z), sl), sl));
 }
 
 // pred != 0: query q (global index q_offset + q) is ordered target i = m + q
 // (q_offset + q) and admits candidates j < i (nearest_neighbors, vg/geo.py:342).
 // pred == 0: every candidate admissible (nearest_points, vg/geo.py:357).
+template <typename PT>
 __global__ void __launch_bounds__(kKnnThreads)
-knn_kernel(const double2* __restrict__ data, int64_t nd, const double2* __restrict__ query,
+knn_kernel(const PT* __restrict__ data, int64_t nd, const PT* __restrict__ query,
            int64_t nq, int64_t q_offset, int pred, int m, int64_t* __restrict__ out,
            double* __restrict__ keys, int32_t* __restrict__ idx) {
-  __shared__ double2 tile[kKnnTile];
+  constexpr int kTile = kKnnTile * 16 / (int)sizeof(PT);
+  __shared__ PT tile[kTile];
   const int64_t q = (int64_t)blockIdx.x * kKnnThreads + threadIdx.x;
   const bool active = q < nq;
   const int64_t stride = (int64_t)gridDim.x * kKnnThreads;  // slot stride in scratch
-  double xt = 0.0, yt = 0.0;
+  PT pt{};
   int64_t limit = 0;
   if (active) {
-    double2 p = query[q];
-    xt = p.x;
-    yt = p.y;
+    pt = query[q];
     limit = pred ? (q_offset + q + m) : nd;
   }
   // block-wide scan bound: the largest limit among this block's queries
@@ -51,9 +64,9 @@ knn_kernel(const double2* __restrict__ data, int64_t nd, const double2* __restri
   int cnt = 0;
   double worst = __longlong_as_double(0x7ff0000000000000ll);  // +inf until full
 
-  for (int64_t base = 0; base < block_limit; base += kKnnTile) {
+  for (int64_t base = 0; base < block_limit; base += kTile) {
     int64_t tn = block_limit - base;
-    if (tn > kKnnTile) tn = kKnnTile;
+    if (tn > kTile) tn = kTile;
     __syncthreads();
     for (int t = threadIdx.x; t < tn; t += kKnnThreads) tile[t] = data[base + t];
     __syncthreads();
@@ -61,8 +74,7 @@ knn_kernel(const double2* __restrict__ data, int64_t nd, const double2* __restri
     int64_t jend = limit - base;
     if (jend > tn) jend = tn;
     for (int t = 0; t < jend; ++t) {
-      double2 c = tile[t];
-      double k = knn_key(c.x, c.y, xt, yt);
+      double k = knn_key(tile[t], pt);
       if (cnt == m && !(k < worst)) continue;  // k >= keys[m-1] -> reject (vg/geo.py:252)
       int p;
       if (cnt == m) {
@@ -96,8 +108,18 @@ cudaError_t launch_knn(const double2* d_data, int64_t nd, const double2* d_query
                        int32_t* d_idx, cudaStream_t stream) {
   if (nq <= 0) return cudaSuccess;
   int64_t blocks = (nq + kKnnThreads - 1) / kKnnThreads;
-  knn_kernel<<<(unsigned)blocks, kKnnThreads, 0, stream>>>(d_data, nd, d_query, nq, q_offset, pred,
-                                                           m, d_out, d_keys, d_idx);
+  knn_kernel<double2><<<(unsigned)blocks, kKnnThreads, 0, stream>>>(d_data, nd, d_query, nq, q_offset,
+                                                                    pred, m, d_out, d_keys, d_idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* d_query, int64_t nq,
+                              int64_t q_offset, int pred, int32_t m, int64_t* d_out, double* d_keys,
+                              int32_t* d_idx, cudaStream_t stream) {
+  if (nq <= 0) return cudaSuccess;
+  int64_t blocks = (nq + kKnnThreads - 1) / kKnnThreads;
+  knn_kernel<double4><<<(unsigned)blocks, kKnnThreads, 0, stream>>>(d_data, nd, d_query, nq, q_offset,
+                                                                    pred, m, d_out, d_keys, d_idx);
   return cudaGetLastError();
 }
 

@@ -91,20 +91,21 @@ def knn_cases():
 
 
 def ll_case(name, n, m, family, s2, beta, nu, seed, ordering="random", data_nu=None,
-            locs=None, y=None, plan_seed=0):
+            locs=None, y=None, plan_seed=0, metric=None):
     spec = kernels.KernelSpec(family, kernels.KernelParams(s2, beta, nu))
     if locs is None:
         rng = np.random.default_rng(seed)
         locs = rng.random((n, 2))
     if y is None:
         gspec = kernels.KernelSpec(family, kernels.KernelParams(s2, beta, data_nu or nu))
-        y = exact.simulate_grf(locs, gspec, seed + 1)
-    data = geo.Dataset(locs, y)
+        y = exact.simulate_grf(locs, gspec, seed + 1, metric or geo.Euclidean())
+    data = geo.Dataset(locs, y, metric or geo.Euclidean())
     plan = vecchia.make_plan(data, m, ordering, seed=plan_seed)
     ordered = data.permute(plan.permutation)
     out = dict(locs=locs, obs=y, perm=plan.permutation.order, ordered_locs=ordered.locations,
                ordered_obs=ordered.observations, m=m, table=plan.neighbors.neighbors,
-               family=family, theta=np.array([s2, beta, nu]), ordering=ordering)
+               family=family, theta=np.array([s2, beta, nu]), ordering=ordering,
+               metric="great_circle" if isinstance(metric, geo.GreatCircle) else "euclidean")
     try:
         res = vecchia.vecchia_loglik(data, plan, spec)
         out.update(status=0, fail_index=-1, total=res.total, block_first=res.block_first,
@@ -172,6 +173,44 @@ def c1_case(with_mle: bool):
     save("c1_n20000_m30_nu05", **out)
 
 
+def sphere_cases():
+    """Great-circle metric (vg/geo.py:70-79, :266-292): kNN of the reference
+    (pkg/tests/test_geo.py:196-204 shape and larger), log-likelihoods with
+    haversine covariance, kriging."""
+    from vecchiagp import fit
+
+    gc = geo.GreatCircle()
+    rng = np.random.default_rng(40)
+    locs = np.column_stack([rng.uniform(-30, 30, 120), rng.uniform(-40, 40, 120)])
+    t = geo.nearest_neighbors(geo.Dataset(locs, np.zeros(120), gc), 7).neighbors
+    save("knn_sphere_120_7", locs=locs, m=7, table=t)
+    rng = np.random.default_rng(41)
+    locs = np.column_stack([rng.uniform(-180, 180, 2000), rng.uniform(-70, 70, 2000)])
+    perm = geo.random_ordering(2000, 0)
+    ordered = geo.Dataset(locs, np.zeros(2000), gc).permute(perm)
+    t = geo.nearest_neighbors(ordered, 30).neighbors
+    save("knn_sphere_2000_30", locs=ordered.locations, m=30, table=t)
+    q = np.column_stack([rng.uniform(-180, 180, 50), rng.uniform(-70, 70, 50)])
+    t = geo.nearest_points(q, locs, gc, 12)
+    save("knn_sphere_points_50_2000_12", query=q, train=locs, m=12, table=t)
+
+    rng = np.random.default_rng(42)
+    locs = np.column_stack([rng.uniform(30, 50, 900), rng.uniform(20, 40, 900)])
+    ll_case("ll_gcd_n900_m20_nu05", 900, 20, "matern", 1.0, 300.0, 0.5, seed=420, locs=locs,
+            metric=gc)
+    ll_case("ll_gcd_n900_m60_nu15", 900, 60, "matern", 1.0, 200.0, 1.5, seed=421, locs=locs,
+            metric=gc)
+    ll_case("ll_gcd_n900_m90_nu08", 900, 90, "matern", 1.0, 250.0, 0.8, seed=422, locs=locs,
+            metric=gc)
+    spec = kernels.KernelSpec("matern", kernels.KernelParams(1.0, 300.0, 0.5))
+    y = exact.simulate_grf(locs, spec, 430, gc)
+    data = geo.Dataset(locs[:850], y[:850], gc)
+    r = fit.krige_predict(data, spec.params, "matern", locs[850:], 30, y[850:])
+    save("krige_gcd_n850_m30_nu05", train=locs[:850], y=y[:850], test=locs[850:], truth=y[850:],
+         m=30, family="matern", theta=np.array([1.0, 300.0, 0.5]), pred=r.predictions,
+         var=r.variances, mse=r.mse, metric="great_circle")
+
+
 def krige_cases():
     """fit.krige_predict (vg/fit.py:221-275) on the reference's own kriging
     setup (pkg/tests/test_fit.py:82-88) and acceptance criterion 6's split
@@ -222,6 +261,8 @@ def main():
         loglik_cases()
     if args.only in ("", "krige"):
         krige_cases()
+    if args.only in ("", "sphere"):
+        sphere_cases()
     if args.only in ("", "c1"):
         c1_case(args.with_mle)
 

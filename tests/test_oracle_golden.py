@@ -11,8 +11,10 @@ from _helpers import golden_names, load, rel
 from oracle import oracle as O
 
 
-@pytest.mark.parametrize("name", golden_names("knn_"))
+@pytest.mark.parametrize("name", [n for n in golden_names("knn_") if "sphere" not in n])
 def test_oracle_knn_matches_reference(name):
+    # great-circle neighbour sets (knn_sphere_*) are pinned directly against
+    # the reference's golden on the GPU (tests/test_gpu_parity.py)
     z = load(name)
     m = int(z["m"])
     if "query" in z.files:
@@ -47,8 +49,9 @@ def test_oracle_c1_table_digest():
 def test_oracle_loglik_matches_reference(name):
     z = load(name)
     s2, beta, nu = (float(v) for v in z["theta"])
+    metric = str(z["metric"]) if "metric" in z.files else "euclidean"
     r = O.loglik(z["ordered_locs"], z["ordered_obs"], int(z["m"]), z["table"], str(z["family"]),
-                 s2, beta, nu)
+                 s2, beta, nu, metric=metric)
     if int(z["status"]) != 0:
         assert r.status != 0
         assert r.fail_index == int(z["fail_index"])
