@@ -231,7 +231,9 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     const bool big_c = big_supported(p->m, cp.kind) && cached && scratch_ok;
     const bool big_n = big_supported(p->m, cp.kind) && eu && scratch_ok;
     int v = p->force_variant;
-    if (v < 0) v = fast_c ? 8 : (fast_n ? 7 : (big_c ? 12 : (big_n ? 11 : 0)));
+    // (the CTA-per-block kernel is faster computing Euclidean distances than
+    // streaming them: profiles/r01_sweep_c3_n250k.jsonl)
+    if (v < 0) v = fast_c ? 8 : (fast_n ? 7 : (big_n ? 11 : (big_c ? 12 : 0)));
     const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
                     ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
@@ -576,7 +578,10 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
       rc = dalloc(&p->d_work, p->work_doubles);
     }
   }
-  if (!rc && nrest > 0 && big_supported(m, kMatern15)) {
+  // distance cache where it pays: the warp-specialised kernel (m + 2 <= 64)
+  // and great-circle plans (haversine per entry would dominate)
+  if (!rc && nrest > 0 && big_supported(m, kMatern15) &&
+      (dmma_supported(m, kMatern15) || metric == VGP_METRIC_GREAT_CIRCLE)) {
     // distance cache: on unless VGP_DCACHE=0, and only when it fits in half
     // of the free device memory
     const char* env = std::getenv("VGP_DCACHE");

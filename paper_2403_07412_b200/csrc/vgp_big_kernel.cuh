@@ -7,8 +7,8 @@
 // m v_e, row m+1 yJ, zero padding) is factored left-looking over 8-wide tile
 // columns:
 //
-//   column   the tiles (I, c), I >= c, are dealt to the warps in groups of
-//            kGroup; each tile is generated (lean FP64 Matern) and updated
+//   column   the tiles (I, c), I >= c, are dealt to the warps round-robin,
+//            kGroup at a time; each tile is generated (lean FP64 Matern) and updated
 //            with every earlier tile column's L, mma.sync.m8n8k4.f64 (SASS
 //            DMMA.8x8x4), kGroup independent accumulators per warp;
 //   diagonal warp 0 factors the 8x8 diagonal tile (one rsqrt / shuffle pivot
@@ -124,11 +124,13 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
     for (int c = 0; c < NC; ++c) {
       const bool lastc = (c == NC - 1);
       // ================= column c: generate + left-looking DMMA update =================
-      for (int I0 = c + warp * kGroup; I0 < NT; I0 += kWarps * kGroup) {
+      // tiles dealt round-robin (warp w: c + w, c + w + 4, ...) in groups of
+      // kGroup, so the warps stay balanced as the column shortens
+      for (int I0 = c + warp; I0 < NT; I0 += kWarps * kGroup) {
         double acc[kGroup][2];
 #pragma unroll
         for (int g = 0; g < kGroup; ++g) {
-          const int I = I0 + g;
+          const int I = I0 + g * kWarps;
           acc[g][0] = acc[g][1] = 0.0;
           if (I < NT) {
             const int i = 8 * I + r;
@@ -160,7 +162,8 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
           double2 a[kGroup];
 #pragma unroll
           for (int g = 0; g < kGroup; ++g)
-            a[g] = I0 + g < NT ? ld2(tile(I0 + g, k) + chunk_off(r, q)) : make_double2(0.0, 0.0);
+            a[g] = I0 + g * kWarps < NT ? ld2(tile(I0 + g * kWarps, k) + chunk_off(r, q))
+                                        : make_double2(0.0, 0.0);
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
@@ -170,7 +173,7 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
         }
 #pragma unroll
         for (int g = 0; g < kGroup; ++g)
-          if (I0 + g < NT) st2(tile(I0 + g, c) + chunk_off(r, q), acc[g][0], acc[g][1]);
+          if (I0 + g * kWarps < NT) st2(tile(I0 + g * kWarps, c) + chunk_off(r, q), acc[g][0], acc[g][1]);
       }
       __syncthreads();
 
