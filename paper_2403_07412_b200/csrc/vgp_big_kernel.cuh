@@ -7,8 +7,8 @@
 // m v_e, row m+1 yJ, zero padding) is factored left-looking over 8-wide tile
 // columns:
 //
-//   column   the tiles (I, c), I >= c, are dealt to the warps round-robin,
-//            kGroup at a time; each tile is generated (lean FP64 Matern) and updated
+//   column   (look-ahead: during column c's diagonal phase) the tiles (I, c+1)
+//            are dealt to warps 1..3 round-robin, kGroup at a time; each tile is generated (lean FP64 Matern) and updated
 //            with every earlier tile column's L, mma.sync.m8n8k4.f64 (SASS
 //            DMMA.8x8x4), kGroup independent accumulators per warp;
 //   diagonal warp 0 factors the 8x8 diagonal tile (one rsqrt / shuffle pivot
@@ -121,62 +121,98 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
     fj = -1;
     __syncthreads();
 
-    for (int c = 0; c < NC; ++c) {
-      const bool lastc = (c == NC - 1);
-      // ================= column c: generate + left-looking DMMA update =================
-      // tiles dealt round-robin (warp w: c + w, c + w + 4, ...) in groups of
-      // kGroup, so the warps stay balanced as the column shortens
-      for (int I0 = c + warp; I0 < NT; I0 += kWarps * kGroup) {
-        double acc[kGroup][2];
+    // tile column J of the block: generate the tiles (I, J), I >= J, dealt
+    // round-robin over warps [w0, w0 + nw) in groups of kGroup (inactive
+    // slots issue nothing), apply L of tile columns k <= kmax with DMMA and
+    // stage them (natural column order)
+    auto column_work = [&](const int J, const int kmax, const int w0, const int nw) {
+        for (int I0 = J + (warp - w0); I0 < NT; I0 += nw * kGroup) {
+          double acc[kGroup][2];
 #pragma unroll
-        for (int g = 0; g < kGroup; ++g) {
-          const int I = I0 + g * kWarps;
-          acc[g][0] = acc[g][1] = 0.0;
-          if (I < NT) {
-            const int i = 8 * I + r;
-            double v0, v1;
-            if (CACHE) {
-              const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, c, NT) * 64 + chunk_off(r, q)));
-              v0 = cov_any<KIND>(dv.x, cp, tab, Bt);
-              v1 = cov_any<KIND>(dv.y, cp, tab, Bt);
-            } else {
-              const double2 pa = XY[i < P ? i : 0];
-              const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * c + 2 * q);
-              double dx = pa.x - pb.x, dy = pa.y - pb.y;
-              v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
-              dx = pa.x - pb.z;
-              dy = pa.y - pb.w;
-              v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
+          for (int g = 0; g < kGroup; ++g) {
+            const int I = I0 + g * nw;
+            acc[g][0] = acc[g][1] = 0.0;
+            if (I < NT) {
+              const int i = 8 * I + r;
+              double v0, v1;
+              if (CACHE) {
+                const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, J, NT) * 64 + chunk_off(r, q)));
+                v0 = cov_any<KIND>(dv.x, cp, tab, Bt);
+                v1 = cov_any<KIND>(dv.y, cp, tab, Bt);
+              } else {
+                const double2 pa = XY[i < P ? i : 0];
+                const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * J + 2 * q);
+                double dx = pa.x - pb.x, dy = pa.y - pb.y;
+                v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
+                dx = pa.x - pb.z;
+                dy = pa.y - pb.w;
+                v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
+              }
+              if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
+                const double2 ov = ld2(O + 8 * J + 2 * q);
+                v0 = i == m + 1 ? ov.x : 0.0;
+                v1 = i == m + 1 ? ov.y : 0.0;
+              }
+              acc[g][0] = v0;
+              acc[g][1] = v1;
             }
-            if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
-              const double2 ov = ld2(O + 8 * c + 2 * q);
-              v0 = i == m + 1 ? ov.x : 0.0;
-              v1 = i == m + 1 ? ov.y : 0.0;
-            }
-            acc[g][0] = v0;
-            acc[g][1] = v1;
           }
-        }
-        for (int k = 0; k < c; ++k) {
-          const double2 b = ld2(tile(c, k) + chunk_off(r, q));
-          double2 a[kGroup];
-#pragma unroll
-          for (int g = 0; g < kGroup; ++g)
-            a[g] = I0 + g * kWarps < NT ? ld2(tile(I0 + g * kWarps, k) + chunk_off(r, q))
-                                        : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
+          // active tiles of this group (warp-uniform): inactive slots issue no
+          // loads and no DMMAs
+          const int ng = min(kGroup, (NT - 1 - I0) / nw + 1);
+          // tile (I, k) at colbase(k) + I, colbase(k) = k NT - k (k+1) / 2 (column-major)
+          const double* col = T + chunk_off(r, q);
+          for (int k = 0; k <= kmax; col += (size_t)(NT - k) * 64, ++k) {
+            const double2 b = ld2(col + (size_t)(J - k) * 64);
+            double2 a[kGroup];
 #pragma unroll
             for (int g = 0; g < kGroup; ++g)
-              mma(acc[g][0], acc[g][1], neg(kk ? a[g].y : a[g].x), kk ? b.y : b.x);
-          }
-        }
+              if (g < ng) a[g] = ld2(col + (size_t)(I0 + g * nw - k) * 64);
 #pragma unroll
-        for (int g = 0; g < kGroup; ++g)
-          if (I0 + g * kWarps < NT) st2(tile(I0 + g * kWarps, c) + chunk_off(r, q), acc[g][0], acc[g][1]);
+            for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+              for (int g = 0; g < kGroup; ++g)
+                if (g < ng) mma(acc[g][0], acc[g][1], neg(kk ? a[g].y : a[g].x), kk ? b.y : b.x);
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g)
+            if (I0 + g * nw < NT) st2(tile(I0 + g * nw, J) + chunk_off(r, q), acc[g][0], acc[g][1]);
+        }
+    };
+    // the last left-looking step of tile column J: reload, apply L of column
+    // k, stage (tiles dealt round-robin over all warps)
+    auto column_finish = [&](const int J, const int k) {
+      const double* col = T + (size_t)tidx(k, k, NT) * 64 + chunk_off(r, q);
+      const double2 b = ld2(col + (size_t)(J - k) * 64);
+      for (int I = J + warp; I < NT; I += kWarps) {
+        double* tp = tile(I, J) + chunk_off(r, q);
+        const double2 v = ld2(tp);
+        const double2 a = ld2(col + (size_t)(I - k) * 64);
+        double a0 = v.x, a1 = v.y;
+        mma(a0, a1, neg(a.x), b.x);
+        mma(a0, a1, neg(a.y), b.y);
+        st2(tp, a0, a1);
       }
-      __syncthreads();
+    };
 
+    // left-looking over tile columns with look-ahead: while warp 0 factors
+    // the diagonal tile of column c, warps 1..3 generate column c + 1 and
+    // apply every earlier column but c; after the row solve of column c one
+    // DMMA step finishes column c + 1
+    // (global-memory tiles, m >~ 230: no look-ahead, the extra reload pass
+    // costs more in L2 than the overlap gains)
+    constexpr bool kLookAhead = !GT;
+    column_work(0, -1, 0, kWarps);
+    __syncthreads();
+    for (int c = 0; c < NC; ++c) {
+      const bool lastc = (c == NC - 1);
+      if (kLookAhead) {
+        if (warp != 0 && !lastc) column_work(c + 1, c - 1, 1, kWarps - 1);
+      } else if (c > 0) {
+        column_work(c, c - 1, 0, kWarps);
+        __syncthreads();
+      }
       // ================= diagonal tile (warp 0) =================
       if (warp == 0) {
         const int R0 = 8 * c;
@@ -305,6 +341,10 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
         }
       }
       __syncthreads();
+      if (kLookAhead) {
+        column_finish(c + 1, c);
+        __syncthreads();
+      }
     }
   }
 }
