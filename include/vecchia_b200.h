@@ -80,6 +80,15 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
 int vgp_knn_sphere(int device, const double* data3, int64_t nd, const double* query3, int64_t nq,
                    int32_t m, int predecessors, int64_t* neighbors);
 
+/* Exact maxmin ordering (BASELINE config 5; new — the reference's orderings
+ * are random / Morton / identity, vg/vecchia.py:37, vg/geo.py:47-91).
+ * order[0] = first (the caller passes the point nearest the centroid); then
+ * repeatedly the unselected point with the largest squared Euclidean
+ * distance dx*dx + dy*dy (rounded, no FMA) to the selected set, ties to the
+ * smallest index.  order: (n,) int64 permutation.  One cooperative launch,
+ * n <= 6553600 points (VGP_E_UNSUPPORTED beyond). */
+int vgp_maxmin_order(int device, const double* locations, int64_t n, int64_t first, int64_t* order);
+
 /* Replaces geo.nearest_points (vg/geo.py:350-358): unrestricted m nearest
  * data points per query row (kriging). neighbors: (nq, m) int64. */
 int vgp_knn_points(int device, const double* query, int64_t nq, const double* data, int64_t nd,

@@ -129,6 +129,32 @@ def knn_pred_bruteforce(locs, m: int) -> np.ndarray:
 
 # ---------------------------------------------------------------- kernels
 
+def maxmin_order(locs, first: int) -> np.ndarray:
+    """Brute-force exact maxmin ordering (checker for vgp_maxmin_order).
+
+    PARITY UNPINNED BY THE REFERENCE: the reference has no maxmin ordering
+    (vg/vecchia.py:37 lists random / Morton / identity); this restates the
+    definition (Guinness 2018) with the device's arithmetic: squared distance
+    (x - cx)**2 + (y - cy)**2 evaluated as rounded dx*dx + dy*dy, argmax with
+    ties to the smallest index.  O(n^2); keep n to a few ten thousand.
+    """
+    locs = np.asarray(locs, dtype=np.float64)
+    n = locs.shape[0]
+    x, y = locs[:, 0].copy(), locs[:, 1].copy()
+    dist = np.full(n, np.inf)
+    order = np.empty(n, dtype=np.int64)
+    cur = int(first)
+    for t in range(n):
+        order[t] = cur
+        dist[cur] = -1.0
+        dx = x - x[cur]
+        dy = y - y[cur]
+        d = dx * dx + dy * dy
+        np.minimum(dist, np.where(dist < 0.0, dist, d), out=dist)
+        cur = int(np.argmax(dist))  # first index of the maximum
+    return order
+
+
 def matern_cov(d, sigma_sq: float, beta: float, nu: float) -> np.ndarray:
     """vg/kernels.py:59-82 restated (scipy kv/gamma for general nu)."""
     from scipy.special import gamma as _gamma

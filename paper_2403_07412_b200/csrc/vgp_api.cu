@@ -362,6 +362,43 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
   return rc;
 }
 
+int vgp_maxmin_order(int device, const double* locations, int64_t n, int64_t first, int64_t* order) {
+  if (!locations || !order) return fail(VGP_E_INVALID, "null pointer");
+  if (n < 1) return fail(VGP_E_INVALID, "need n >= 1");
+  if (first < 0 || first >= n) return fail(VGP_E_INVALID, "first index out of range");
+  int rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  if (n > maxmin_capacity())
+    return fail(VGP_E_UNSUPPORTED, "maxmin ordering holds at most " + std::to_string(maxmin_capacity()) + " points");
+  double bbox[4] = {locations[0], locations[0], locations[1], locations[1]};
+  for (int64_t i = 0; i < n; ++i) {
+    const double x = locations[2 * i], y = locations[2 * i + 1];
+    if (!(x == x) || !(y == y)) return fail(VGP_E_INVALID, "NaN location");
+    bbox[0] = std::min(bbox[0], x);
+    bbox[1] = std::max(bbox[1], x);
+    bbox[2] = std::min(bbox[2], y);
+    bbox[3] = std::max(bbox[3], y);
+  }
+  cudaStream_t s;
+  VGP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double2* d_pts = nullptr;
+  int64_t* d_order = nullptr;
+  rc = dalloc(&d_pts, n);
+  if (!rc) rc = dalloc(&d_order, n);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
+  if (!rc && e == cudaSuccess) e = launch_maxmin(d_pts, n, first, bbox, d_order, s);
+  if (!rc && e == cudaSuccess)
+    e = cudaMemcpyAsync(order, d_order, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s);
+  if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("maxmin: ") + cudaGetErrorString(e));
+  cudaFree(d_pts);
+  cudaFree(d_order);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
 int vgp_knn_sphere(int device, const double* data3, int64_t nd, const double* query3, int64_t nq,
                    int32_t m, int predecessors, int64_t* neighbors) {
   if (!data3 || !neighbors || (!predecessors && !query3)) return fail(VGP_E_INVALID, "null pointer");

@@ -113,6 +113,13 @@ cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* 
                               int64_t q_offset, int pred, int32_t m, int64_t* d_out, double* d_keys,
                               int32_t* d_idx, cudaStream_t stream);
 
+// Exact maxmin ordering (vgp_maxmin.cu): order[t] for t < n, starting at
+// `first`; bbox = (x0, x1, y0, y1) of the points; at most maxmin_capacity()
+// points (one cluster holds every chunk's metadata in shared memory).
+int64_t maxmin_capacity();
+cudaError_t launch_maxmin(const double2* d_pts, int64_t n, int64_t first, const double bbox[4],
+                          int64_t* d_order, cudaStream_t stream);
+
 // Permute raw (x, y, obs) rows into ordered double4 points.
 cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t n,
                            double4* d_pts, cudaStream_t stream);

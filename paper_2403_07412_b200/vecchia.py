@@ -28,7 +28,7 @@ from . import geo, kernels
 
 LOG_2PI = math.log(2.0 * math.pi)
 _REDUCE_CHUNK = 4096
-ORDERINGS = ("random", "morton", "identity")
+ORDERINGS = ("random", "morton", "identity", "maxmin")  # maxmin: new (BASELINE config 5)
 
 
 @dataclass
@@ -69,6 +69,10 @@ def make_plan(dataset: geo.Dataset, m: int, ordering: str = "random", seed: int 
         perm = geo.random_ordering(n, seed)
     elif ordering == "morton":
         perm = geo.morton_ordering(dataset.locations)
+    elif ordering == "maxmin":
+        if isinstance(dataset.metric, geo.GreatCircle):
+            raise ValueError("maxmin ordering is Euclidean only")
+        perm = geo.maxmin_ordering(dataset.locations)
     else:
         perm = geo.Permutation(np.arange(n))
     if n == 1:

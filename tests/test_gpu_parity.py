@@ -440,3 +440,76 @@ def test_sharded_partials_bitwise_on_one_gpu(vg, oracle, world, m, variant):
         acc += send
         dp.close()
     assert ordered_total(acc.cpu().numpy()) == full.total
+
+
+# ---------------------------------------------------------------- maxmin ordering (config 5)
+
+def _clustered(rng, n, k=12, scale=0.02):
+    centers = rng.random((k, 2))
+    lab = rng.integers(0, k, n)
+    return centers[lab] + scale * rng.standard_normal((n, 2))
+
+
+@pytest.mark.parametrize("case", ["uniform", "clustered", "lattice", "duplicates", "tiny1", "tiny2",
+                                  "collinear", "uniform_big"])
+def test_maxmin_order_vs_oracle(vg, oracle, case):
+    """Exact maxmin (new: no reference counterpart) against the brute-force
+    restatement with the same arithmetic; bit-exact permutation, including
+    the tie-heavy lattice and duplicate points."""
+    rng = np.random.default_rng(hash(case) % 1000)
+    if case == "uniform":
+        locs = rng.random((3000, 2))
+    elif case == "clustered":
+        locs = _clustered(rng, 6000)
+    elif case == "lattice":
+        g = np.arange(70, dtype=np.float64)
+        locs = np.stack(np.meshgrid(g, g, indexing="ij"), -1).reshape(-1, 2)
+    elif case == "duplicates":
+        base = rng.random((500, 2))
+        locs = base[rng.integers(0, 500, 4000)]
+    elif case == "tiny1":
+        locs = rng.random((1, 2))
+    elif case == "tiny2":
+        locs = rng.random((2, 2))
+    elif case == "collinear":
+        locs = np.stack([rng.random(2500), np.full(2500, 0.25)], -1)
+    else:
+        locs = rng.random((20000, 2))
+    perm = vg.geo.maxmin_ordering(locs)
+    want = oracle.maxmin_order(locs, vg.geo.maxmin_first(locs))
+    np.testing.assert_array_equal(perm.order, want)
+
+
+def test_maxmin_plan_end_to_end(vg, oracle):
+    """Config-5 shape at test size: clustered locations, maxmin ordering,
+    GPU kNN, fused likelihood vs the oracle at 1e-9."""
+    rng = np.random.default_rng(5)
+    n, m, nu, beta = 20000, 30, 0.8, 0.05
+    locs = _clustered(rng, n)
+    plan = vg.make_plan(vg.Dataset(locs, np.zeros(n)), m, "maxmin")
+    assert plan.ordering == "maxmin"
+    np.testing.assert_array_equal(plan.permutation.order,
+                                  oracle.maxmin_order(locs, vg.geo.maxmin_first(locs)))
+    y = rng.standard_normal(n)
+    data = vg.Dataset(locs, y)
+    ordered = data.permute(plan.permutation)
+    ref = oracle.loglik(ordered.locations, ordered.observations, m, plan.neighbors.neighbors,
+                        "matern", 1.0, beta, nu)
+    res = vg.vecchia_loglik(data, plan, vg.KernelSpec("matern", vg.KernelParams(1.0, beta, nu)))
+    assert ref.status == 0
+    assert rel(res.total, ref.total) <= TOL_TOTAL
+
+
+def test_maxmin_large_is_permutation_and_monotone(vg):
+    """n = 500k (beyond the oracle): a permutation whose selection distances
+    (squared distance of order[t] to order[:t], checked on a sample of t via
+    the exact predecessor kNN with m = 1) never increase."""
+    rng = np.random.default_rng(9)
+    n = 500_000
+    locs = _clustered(rng, n, k=40, scale=0.05)
+    order = vg.geo.maxmin_ordering(locs).order
+    assert np.array_equal(np.sort(order), np.arange(n))
+    ordered = locs[order]
+    nn = vg.geo.nearest_neighbors(vg.Dataset(ordered, np.zeros(n)), 1).neighbors[:, 0]
+    d = ((ordered[1:] - ordered[nn]) ** 2).sum(1)
+    assert np.all(np.diff(d) <= 1e-12 * d[:-1] + 1e-300)

@@ -208,3 +208,50 @@ class TestDetrendSqrt:
             fit.krige_predict(data, theta, "matern", np.zeros((3, 2)), m=11)
         with pytest.raises(ValueError):
             fit.krige_predict(data, theta, "matern", np.zeros((3, 3)), m=2)
+
+
+class TestMaxminHost:
+    """The maxmin checker (oracle) against a literal restatement of the
+    definition, and the host-side pieces of the device ordering."""
+
+    @staticmethod
+    def _literal(locs, first):
+        n = len(locs)
+        chosen = [first]
+        rest = set(range(n)) - {first}
+        while rest:
+            best, bi = -1.0, None
+            for i in sorted(rest):
+                d = min((locs[i, 0] - locs[j, 0]) * (locs[i, 0] - locs[j, 0])
+                        + (locs[i, 1] - locs[j, 1]) * (locs[i, 1] - locs[j, 1]) for j in chosen)
+                if d > best:
+                    best, bi = d, i
+            chosen.append(bi)
+            rest.remove(bi)
+        return np.array(chosen)
+
+    @pytest.mark.parametrize("seed", [0, 1, 2])
+    def test_oracle_matches_definition(self, seed):
+        from oracle import oracle as O
+
+        rng = np.random.default_rng(seed)
+        locs = rng.random((60, 2))
+        if seed == 2:  # lattice with ties and a duplicate
+            g = np.arange(7.0)
+            locs = np.stack(np.meshgrid(g, g, indexing="ij"), -1).reshape(-1, 2)
+            locs = np.vstack([locs, locs[:3]])
+        first = geo.maxmin_first(locs)
+        np.testing.assert_array_equal(O.maxmin_order(locs, first), self._literal(locs, first))
+
+    def test_first_is_nearest_centroid(self):
+        locs = np.array([[0.0, 0.0], [1.0, 1.0], [0.4, 0.6], [0.6, 0.4]])
+        assert geo.maxmin_first(locs) == 2  # tie between 2 and 3 -> smallest index
+
+    def test_validation_before_device(self):
+        with pytest.raises(ValueError):
+            geo.maxmin_ordering(np.zeros((3, 3)))
+        with pytest.raises(ValueError):
+            geo.maxmin_ordering(np.array([[0.0, np.nan]]))
+        with pytest.raises(ValueError):
+            vecchia.make_plan(geo.Dataset(np.zeros((3, 2)), np.zeros(3), geo.GreatCircle()), 1, "maxmin")
+        assert "maxmin" in vecchia.ORDERINGS
