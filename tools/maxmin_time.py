@@ -12,7 +12,7 @@ import paper_2403_07412_b200 as vg
 
 sizes = [int(s) for s in sys.argv[1:]] or [250_000, 1_000_000, 2_000_000]
 for n in sizes:
-    for kind in ("clustered", "uniform"):
+    for kind in (("uniform",) if __import__("os").environ.get("MM_UNIFORM") else ("clustered", "uniform")):
         rng = np.random.default_rng(n)
         if kind == "uniform":
             locs = rng.random((n, 2))
