@@ -232,8 +232,14 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     const bool big_n = big_supported(p->m, cp.kind) && eu && scratch_ok;
     int v = p->force_variant;
     // (the CTA-per-block kernel is faster computing Euclidean distances than
-    // streaming them: profiles/r01_sweep_c3_n250k.jsonl)
-    if (v < 0) v = fast_c ? 8 : (fast_n ? 7 : (big_n ? 11 : (big_c ? 12 : 0)));
+    // streaming them for the closed forms, profiles/r01_sweep_c3_n250k.jsonl;
+    // for general nu / power exponential, where covariance generation
+    // dominates, streaming them is 1.6x faster, profiles/r01_c5_general_nu.txt)
+    const bool big_prefer_cache = cp.kind >= kMaternGen;
+    if (v < 0)
+      v = fast_c ? 8
+                 : (fast_n ? 7
+                           : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
     const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
                     ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");

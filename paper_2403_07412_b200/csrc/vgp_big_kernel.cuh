@@ -58,6 +58,15 @@ __host__ __device__ inline int64_t tile_doubles(int m) {
   return (int64_t)ntri(nt) * 64;
 }
 
+// General-nu Matern: s2 2^(1-nu)/Gamma(nu) u^nu K_nu(u), u = d / beta
+// (vg/kernels.py:75-81).  Not inlined: the kernel evaluates covariances at
+// 2 * kGroup unrolled sites, and eight inlined copies of the Bessel K
+// iteration overflow the instruction cache (profiles/r01_ncu_c5_*.txt).
+__device__ __noinline__ double matern_gen(double d, const CovParams& cp, const double* btab) {
+  const double u = d / cp.beta;
+  return cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k_tab(cp, u, btab);
+}
+
 // covariance at distance d: lean closed forms, or the reference expression
 // (general-nu Matern via the device Bessel K_nu, power exponential;
 // vg/kernels.py:59-91) with C(0) = sigma^2 exactly (d below 1e-100: the
@@ -67,16 +76,12 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
                                           const double* btab) {
   if (KIND <= kMatern25) return cov_lean<KIND>(d, cp.inv_beta, tab);
   if (d < 1e-100) return cp.s2;
-  if (KIND == kMaternGen) {
-    // s2 2^(1-nu)/Gamma(nu) u^nu K_nu(u), u = d / beta (vg/kernels.py:75-81)
-    const double u = d / cp.beta;
-    return cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k_tab(cp, u, btab);
-  }
+  if (KIND == kMaternGen) return matern_gen(d, cp, btab);
   return cov_ref(cp, d);
 }
 
 template <int KIND, bool CACHE, bool GT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, KIND == kMaternGen ? 4 : 1)
 loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
                   int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,

@@ -113,13 +113,15 @@ def test_loglik_vs_reference_golden(vg, name, variant):
         pytest.skip("warp-DMMA variants cover m + 2 <= 64 closed-form Matern only")
     if variant in (1, 2, 3, 7, 11) and not plane:
         pytest.skip("distances computed in the kernel are Euclidean (great circle: cached variants)")
-    if variant == 12 and plane and not fast:
+    cache = not plane or int(z["m"]) + 2 <= 64
+    if variant == 12 and not cache:
         pytest.skip("large-m Euclidean plans carry no distance cache")
     plan.device_plan().set_variant(variant)
     res = vg.vecchia_loglik(data, plan, spec)
     # the cache exists for m + 2 <= 64 and for great-circle plans; the large-m
-    # kernel computes Euclidean distances
-    auto = 8 if fast else (11 if plane else 12)
+    # kernel computes Euclidean distances for the closed forms and streams
+    # the cache for general nu / power exponential when there is one
+    auto = 8 if fast else (12 if cache and (not plane or not closed) else 11)
     assert plan.device_plan().kernel_variant == (variant if variant >= 0 else auto)
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL
     assert rel(res.block_first, float(z["block_first"])) <= TOL_TOTAL
