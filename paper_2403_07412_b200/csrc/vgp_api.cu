@@ -236,10 +236,15 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     // for general nu / power exponential, where covariance generation
     // dominates, streaming them is 1.6x faster, profiles/r01_c5_general_nu.txt)
     const bool big_prefer_cache = cp.kind >= kMaternGen;
+    // small blocks (m + 2 <= 32): one warp per block with everything in
+    // registers beats warp specialisation (profiles/r01_smallm_variants.txt)
+    const bool small = p->m + 2 <= 32;
     if (v < 0)
-      v = fast_c ? 8
-                 : (fast_n ? 7
-                           : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
+      v = small && fast_n ? 1
+        : small && fast_c ? 4
+        : fast_c ? 8
+        : (fast_n ? 7
+                  : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
     const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
                     ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");

@@ -121,7 +121,9 @@ def test_loglik_vs_reference_golden(vg, name, variant):
     # the cache exists for m + 2 <= 64 and for great-circle plans; the large-m
     # kernel computes Euclidean distances for the closed forms and streams
     # the cache for general nu / power exponential when there is one
-    auto = 8 if fast else (12 if cache and (not plane or not closed) else 11)
+    small = int(z["m"]) + 2 <= 32
+    auto = ((1 if plane else 4) if small else 8) if fast else (
+        12 if cache and (not plane or not closed) else 11)
     assert plan.device_plan().kernel_variant == (variant if variant >= 0 else auto)
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL
     assert rel(res.block_first, float(z["block_first"])) <= TOL_TOTAL
@@ -297,7 +299,7 @@ def test_distance_cache_is_bit_identical(vg, name):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
     dp = plan.device_plan()
-    dp.set_variant(-1)
+    dp.set_variant(4)  # warp-specialised kernel streaming the cache
     a = vg.vecchia_loglik(data, plan, spec)
     cached = dp.info()[8] == 1
     dp.set_variant(3)  # same warp-specialised kernel, distances from coordinates
