@@ -242,6 +242,42 @@ def krige_cases():
              var=r.variances, mse=r.mse)
 
 
+def kl_cases():
+    """exact.exact_loglik / kl_vecchia / simulate_grf / kl_gaussian
+    (vg/exact.py) on the reference's own KL setups (pkg/tests/test_exact.py
+    TestKLVecchia, pkg/tests/test_acceptance.py criteria 3 and 4, smaller)."""
+    from vecchiagp.kernels import KernelParams, KernelSpec
+
+    spec = KernelSpec("matern", KernelParams(1.0, 0.026270, 0.5))
+    locs = np.random.default_rng(8).random((400, 2))
+    data = vecchiagp.Dataset(locs, np.zeros(400))
+    for m in (5, 20, 60, 399):
+        plan = vecchia.make_plan(data, m, "random", seed=3)
+        r = exact.kl_vecchia(locs, plan, spec)
+        save(f"kl_n400_m{m}_random", locs=locs, m=m, ordering="random", plan_seed=3,
+             family="matern", theta=np.array([1.0, 0.026270, 0.5]), kl=r.kl,
+             exact_ll0=r.exact_ll0, vecchia_ll0=r.vecchia_ll0)
+    spec2 = KernelSpec("matern", KernelParams(1.0, 0.078809, 0.5))
+    locs = np.random.default_rng(2024).random((1024, 2))
+    data = vecchiagp.Dataset(locs, np.zeros(1024))
+    for ordering in ("random", "morton"):
+        plan = vecchia.make_plan(data, 30, ordering, seed=1)
+        r = exact.kl_vecchia(locs, plan, spec2)
+        save(f"kl_n1024_m30_{ordering}", locs=locs, m=30, ordering=ordering, plan_seed=1,
+             family="matern", theta=np.array([1.0, 0.078809, 0.5]), kl=r.kl,
+             exact_ll0=r.exact_ll0, vecchia_ll0=r.vecchia_ll0)
+    # exact log-likelihood of simulated fields, general nu and power exponential
+    rng = np.random.default_rng(31)
+    locs = rng.random((700, 2))
+    for fam, th in (("matern", (1.3, 0.06, 1.5)), ("matern", (0.8, 0.05, 0.8)),
+                    ("power_exponential", (1.1, 0.07, 1.2))):
+        sp = KernelSpec(fam, KernelParams(*th))
+        y = exact.simulate_grf(locs, sp, seed=32)
+        ll = exact.exact_loglik(vecchiagp.Dataset(locs, y), sp)
+        save(f"exact_n700_{fam[:6]}_nu{str(th[2]).replace('.', '')}", locs=locs, y=y, family=fam,
+             theta=np.array(th), exact_ll=ll)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--with-mle", action="store_true")
@@ -263,6 +299,8 @@ def main():
         krige_cases()
     if args.only in ("", "sphere"):
         sphere_cases()
+    if args.only in ("", "kl"):
+        kl_cases()
     if args.only in ("", "c1"):
         c1_case(args.with_mle)
 

@@ -153,10 +153,18 @@ def test_ordered_sum_matches_oracle():
     assert vecchia._ordered_sum(a) == O.ordered_sum(a)
 
 
-def test_exact_objective_is_out_of_scope():
+def test_exact_objective_guard_before_device():
+    """The dense objective (vg/fit.py:165-166) keeps the reference's guard:
+    ValueError past max_dense_n, raised before any device work."""
     data = vg.Dataset(np.random.default_rng(0).random((40, 2)), np.zeros(40))
-    with pytest.raises(NotImplementedError):
-        vg.mle_estimate(data, vg.FitConfig(objective="exact"))
+    with pytest.raises(ValueError):
+        vg.mle_estimate(data, vg.FitConfig(objective="exact", max_dense_n=39))
+    from paper_2403_07412_b200 import exact
+
+    with pytest.raises(ValueError):
+        exact.kl_gaussian(np.eye(3), np.eye(4))
+    with pytest.raises(ValueError):
+        exact.exact_loglik(data, vg.KernelSpec("matern", vg.KernelParams(1.0, 0.1, 0.5)), max_n=10)
 
 
 def test_pin_skips_views_and_small_arrays():
