@@ -80,6 +80,19 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
 int vgp_knn_sphere(int device, const double* data3, int64_t nd, const double* query3, int64_t nq,
                    int32_t m, int predecessors, int64_t* neighbors);
 
+/* Replaces vecchia.assemble (vg/vecchia.py:106-166): the materialised
+ * conditioning batches of the unfused stage API (assemble -> _numeric_stage
+ * -> _reduction_stage, as timed by cli.cmd_bench, vg/cli.py:259-263).
+ * locations/observations: ORDERED (n, 2) / (n,); neighbors (n - m, m) int64;
+ * outputs for the n - m + 1 entries: sigma column-major m x m matrices at
+ * stride sigma_stride (>= m*m), v and yj at strides >= m.  Entry 0 is the
+ * joint first block with v = yj = observations[0:m].  Covariances are the
+ * reference expressions (vg/kernels.py:59-91) on the device. */
+int vgp_assemble(int device, const double* locations, const double* observations, int64_t n, int32_t m,
+                 const int64_t* neighbors, int metric, double radius, int family, double sigma_sq,
+                 double beta, double nu, double* sigma, int64_t sigma_stride, double* v, int64_t v_stride,
+                 double* yj, int64_t yj_stride);
+
 /* Exact maxmin ordering (BASELINE config 5; new — the reference's orderings
  * are random / Morton / identity, vg/vecchia.py:37, vg/geo.py:47-91).
  * order[0] = first (the caller passes the point nearest the centroid); then

@@ -373,6 +373,74 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
   return rc;
 }
 
+int vgp_assemble(int device, const double* locations, const double* observations, int64_t n, int32_t m,
+                 const int64_t* neighbors, int metric, double radius, int family, double sigma_sq,
+                 double beta, double nu, double* sigma, int64_t sigma_stride, double* v, int64_t v_stride,
+                 double* yj, int64_t yj_stride) {
+  if (!locations || !observations || !sigma || !v || !yj || !neighbors)
+    return fail(VGP_E_INVALID, "null pointer");
+  if (m < 1 || n <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
+  if (sigma_stride < (int64_t)m * m || v_stride < m || yj_stride < m)
+    return fail(VGP_E_INVALID, "stride smaller than the block size");
+  if (metric != VGP_METRIC_EUCLIDEAN && metric != VGP_METRIC_GREAT_CIRCLE)
+    return fail(VGP_E_INVALID, "unknown metric");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  const int64_t count = n - m + 1;
+  for (int64_t i = 0; i < (n - m) * (int64_t)m; ++i)
+    if (neighbors[i] < 0 || neighbors[i] >= n) return fail(VGP_E_INVALID, "neighbour index out of range");
+  rc = check_device(device);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t s;
+  VGP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // entries per chunk: at most ~256 MB of matrices on the device
+  const int64_t mm = (int64_t)m * m;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(count, (int64_t(32) << 20) / mm));
+  double2* d_pts = nullptr;
+  double *d_obs = nullptr, *d_S = nullptr, *d_v = nullptr, *d_y = nullptr;
+  int64_t* d_nbr = nullptr;
+  rc = dalloc(&d_pts, n);
+  if (!rc) rc = dalloc(&d_obs, n);
+  if (!rc) rc = dalloc(&d_nbr, (size_t)(n - m) * m);
+  if (!rc) rc = dalloc(&d_S, (size_t)chunk * mm);
+  if (!rc) rc = dalloc(&d_v, (size_t)chunk * m);
+  if (!rc) rc = dalloc(&d_y, (size_t)chunk * m);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
+  if (!rc && e == cudaSuccess) e = cudaMemcpyAsync(d_obs, observations, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (!rc && e == cudaSuccess)
+    e = cudaMemcpyAsync(d_nbr, neighbors, sizeof(int64_t) * (n - m) * m, cudaMemcpyHostToDevice, s);
+  for (int64_t e0 = 0; !rc && e == cudaSuccess && e0 < count; e0 += chunk) {
+    const int64_t ne = std::min(chunk, count - e0);
+    e = launch_assemble(d_pts, d_obs, m, d_nbr, e0, ne, metric, metric == VGP_METRIC_GREAT_CIRCLE ? radius : 0.0, cp,
+                        d_S, d_v, d_y, sms, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(sigma + e0 * sigma_stride, sizeof(double) * sigma_stride, d_S, sizeof(double) * mm,
+                            sizeof(double) * mm, ne, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(v + e0 * v_stride, sizeof(double) * v_stride, d_v, sizeof(double) * m,
+                            sizeof(double) * m, ne, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(yj + e0 * yj_stride, sizeof(double) * yj_stride, d_y, sizeof(double) * m,
+                            sizeof(double) * m, ne, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the device chunk is reused
+  }
+  if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("assemble: ") + cudaGetErrorString(e));
+  cudaFree(d_pts);
+  cudaFree(d_obs);
+  cudaFree(d_nbr);
+  cudaFree(d_S);
+  cudaFree(d_v);
+  cudaFree(d_y);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
 int vgp_maxmin_order(int device, const double* locations, int64_t n, int64_t first, int64_t* order) {
   if (!locations || !order) return fail(VGP_E_INVALID, "null pointer");
   if (n < 1) return fail(VGP_E_INVALID, "need n >= 1");

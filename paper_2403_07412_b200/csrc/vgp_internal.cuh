@@ -120,6 +120,11 @@ int64_t maxmin_capacity();
 cudaError_t launch_maxmin(const double2* d_pts, int64_t n, int64_t first, const double bbox[4],
                           int64_t* d_order, cudaStream_t stream);
 
+// Materialised conditioning batches for entries [e0, e0 + ne) (vgp_assemble.cu).
+cudaError_t launch_assemble(const double2* d_pts, const double* d_obs, int m, const int64_t* d_nbr, int64_t e0,
+                            int64_t ne, int metric, double radius, const CovParams& cp, double* d_S,
+                            double* d_v, double* d_y, int num_sms, cudaStream_t s);
+
 // Permute raw (x, y, obs) rows into ordered double4 points.
 cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t n,
                            double4* d_pts, cudaStream_t stream);

@@ -349,3 +349,97 @@ def flop_count(n: int, m: int) -> float:
     blocks = float(n - m + 1)
     fm = float(m)
     return blocks * (fm**3 / 3.0 + 2.0 * fm**2 + 4.0 * fm)
+
+
+# ---------------------------------------------------------------- staged API
+# The reference's three-stage evaluation (vg/vecchia.py:85-214), kept for
+# callers that drive the stages themselves (cli.cmd_bench, vg/cli.py:259-263,
+# and the reference's assemble tests).  Unlike vecchia_loglik, which runs the
+# fused kernel and never materialises a block, this path stores every
+# conditioning block (28.8 GB at n = 1M, m = 60, as the reference does): the
+# blocks are generated on the device (vgp_assemble) and factored / solved by
+# the device batched kernels (batchla, vgp_batch_*).
+
+
+@dataclass
+class BatchWorkspace:
+    """Strided storage for the n - m + 1 conditioning blocks (vg/vecchia.py:85-92)."""
+
+    Sigma: "batchla.StridedMatrixBatch"
+    v: "batchla.StridedVectorBatch"
+    yJ: "batchla.StridedVectorBatch"
+    sigma_diag: "batchla.BatchScalars"
+
+
+def assemble(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.KernelSpec,
+             out: BatchWorkspace | None = None) -> BatchWorkspace:
+    """Populate the conditioning batches of an already-permuted dataset
+    (vg/vecchia.py:106-166) with ``vgp_assemble`` on the GPU.  Passing a
+    previous workspace as ``out`` refills it in place."""
+    from . import batchla
+
+    n, m = dataset.n, plan.m
+    if plan.permutation.n != n:
+        raise ValueError(f"plan built for n={plan.permutation.n}, dataset has n={n}")
+    if not (1 <= m < n):
+        raise ValueError(f"need 1 <= m < n, got m={m}, n={n}")
+    count = n - m + 1
+    if out is None:
+        ws = BatchWorkspace(
+            Sigma=batchla.StridedMatrixBatch.zeros(count, m),
+            v=batchla.StridedVectorBatch.zeros(count, m),
+            yJ=batchla.StridedVectorBatch.zeros(count, m),
+            sigma_diag=batchla.BatchScalars(np.empty(count)),
+        )
+    else:
+        ws = out
+        if ws.Sigma.count != count or ws.Sigma.dim != m:
+            raise ValueError(f"workspace shaped ({ws.Sigma.count}, {ws.Sigma.dim}), need ({count}, {m})")
+    ws.sigma_diag.values[:] = spec.params.sigma_sq
+    metric, radius = _metric_code(dataset.metric)
+    locs = np.ascontiguousarray(dataset.locations, dtype=np.float64)
+    obs = np.ascontiguousarray(dataset.observations, dtype=np.float64)
+    nbr = np.ascontiguousarray(plan.neighbors.neighbors, dtype=np.int64)
+    p = spec.params
+    N.check(N.lib.vgp_assemble(N.current_device(), N.dptr(locs), N.dptr(obs), n, m, N.iptr(nbr), metric,
+                               radius, N.FAMILY_CODES[spec.family], float(p.sigma_sq), float(p.beta),
+                               float(p.nu), N.dptr(ws.Sigma.buffer), ws.Sigma.stride,
+                               N.dptr(ws.v.buffer), ws.v.stride, N.dptr(ws.yJ.buffer), ws.yJ.stride))
+    return ws
+
+
+def _numeric_stage(ws: BatchWorkspace):
+    """Factor, solve and dot every block on the GPU; Sigma is overwritten by
+    its factor (vg/vecchia.py:180-190)."""
+    from . import batchla
+    from .errors import LikelihoodEvaluationError, NonPositiveDefiniteError
+
+    try:
+        lower = batchla.batch_potrf(ws.Sigma)
+    except NonPositiveDefiniteError as exc:
+        raise LikelihoodEvaluationError(exc.batch_index, str(exc)) from exc
+    v_prime = batchla.batch_trsv(lower, ws.v)
+    y_prime = batchla.batch_trsv(lower, ws.yJ)
+    mu_prime = batchla.batch_dot(y_prime, v_prime).values
+    sigma_prime = batchla.batch_dot(v_prime, v_prime).values
+    return lower, mu_prime, sigma_prime
+
+
+def _reduction_stage(ws: BatchWorkspace, ordered_obs: np.ndarray, m: int, lower, mu_prime: np.ndarray,
+                     sigma_prime: np.ndarray) -> LogLikResult:
+    """Per-block log-densities and the ordered total (vg/vecchia.py:193-214),
+    the same O(n) arithmetic the fused kernel's epilogue performs."""
+    from . import batchla
+    from .errors import LikelihoodEvaluationError
+
+    block_first = -batchla.half_log_det(lower.matrix(0)) - 0.5 * mu_prime[0] - 0.5 * m * LOG_2PI
+    mu_new = mu_prime[1:]
+    sigma_new = ws.sigma_diag.values[1:] - sigma_prime[1:]
+    bad = ~(sigma_new > 0.0)
+    if np.any(bad):
+        k = 1 + int(np.argmax(bad))
+        raise LikelihoodEvaluationError(k, f"conditional variance {sigma_new[k - 1]!r} <= 0")
+    resid = np.asarray(ordered_obs, dtype=np.float64)[m:] - mu_new
+    block_rest = -0.5 * (resid * resid / sigma_new + LOG_2PI + np.log(sigma_new))
+    total = block_first + _ordered_sum(block_rest)
+    return LogLikResult(total, block_first, block_rest, mu_new, sigma_new)
