@@ -186,7 +186,7 @@ class DevicePlan:
         bf = np.zeros(1)
         fail = np.full(1, -1, dtype=np.int64)
         if full_result:
-            rest, mu, sg = np.empty(k), np.empty(k), np.empty(k)
+            rest, mu, sg = _RESULTS.take(k), _RESULTS.take(k), _RESULTS.take(k)
             ptrs = (N.dptr(rest), N.dptr(mu), N.dptr(sg))
         else:
             rest = mu = sg = None
@@ -267,6 +267,49 @@ def _pin(arr: np.ndarray) -> None:
 def _unpin(ptr: int) -> None:
     if _PINNED.pop(ptr, None) is not None:
         N.lib.vgp_host_unregister(ctypes.c_void_p(ptr))
+
+
+class _ResultPool:
+    """Page-locked buffers for the per-block results of ``vecchia_loglik``.
+
+    Every call still returns fresh arrays (the reference's contract), but
+    their memory comes from a pool of registered (page-locked) buffers, so
+    the chunked device->host result download runs as DMA instead of through
+    the driver's pageable bounce buffer.  A buffer returns to the pool when
+    the last array (or view) over it is garbage collected: the handed-out
+    array is built over a per-call ctypes object whose finalizer does the
+    return, and numpy views keep that object alive.
+    """
+
+    def __init__(self, keep: int = 6):
+        self.keep = keep
+        self.free: dict = {}  # length -> [raw arrays]
+        self.busy: dict = {}  # id(ctypes holder) -> raw array
+
+    def take(self, k: int) -> np.ndarray:
+        lst = self.free.get(k)
+        if lst:
+            raw = lst.pop()
+        else:
+            raw = np.empty(max(k, 1))
+            if raw.nbytes >= (1 << 20):
+                _pin(raw)
+        holder = (ctypes.c_double * k).from_address(raw.ctypes.data)
+        out = np.ctypeslib.as_array(holder) if k else np.empty(0)
+        self.busy[id(holder)] = raw
+        weakref.finalize(holder, self._give, id(holder), k)
+        return out
+
+    def _give(self, key: int, k: int) -> None:
+        raw = self.busy.pop(key, None)
+        if raw is None:
+            return
+        lst = self.free.setdefault(k, [])
+        if len(lst) < self.keep:
+            lst.append(raw)
+
+
+_RESULTS = _ResultPool()
 
 
 class LikelihoodSession:

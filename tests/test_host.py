@@ -263,3 +263,25 @@ class TestMaxminHost:
         with pytest.raises(ValueError):
             vecchia.make_plan(geo.Dataset(np.zeros((3, 2)), np.zeros(3), geo.GreatCircle()), 1, "maxmin")
         assert "maxmin" in vecchia.ORDERINGS
+
+
+def test_result_pool_reuses_only_dead_buffers():
+    """Per-block results come from a page-locked pool: a buffer is reused
+    only after every array / view over it is gone."""
+    import gc
+
+    pool = vecchia._ResultPool(keep=2)
+    a = pool.take(1000)
+    a[:] = 1.0
+    addr = a.ctypes.data
+    view = a[10:]
+    del a
+    gc.collect()
+    b = pool.take(1000)
+    assert b.ctypes.data != addr  # the view still pins the first buffer
+    del view
+    gc.collect()
+    c = pool.take(1000)
+    assert c.ctypes.data == addr  # now recycled
+    assert c.shape == (1000,) and c.dtype == np.float64
+    assert pool.take(0).shape == (0,)
