@@ -348,6 +348,21 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
   double* d_keys = nullptr;
   int32_t* d_idx = nullptr;
   const int64_t nq = n - m;
+  // grid-pruned search past ~200k points (env VGP_KNN_GRID_MIN overrides);
+  // both paths produce the same table bit for bit
+  int64_t grid_min = 200000;
+  if (const char* env = std::getenv("VGP_KNN_GRID_MIN")) grid_min = std::atoll(env);
+  if (n >= grid_min) {
+    rc = dalloc(&d_pts, n);
+    cudaError_t e = cudaSuccess;
+    if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
+    if (!rc && e == cudaSuccess) e = knn_pred_grid(d_pts, locations, n, m, 32768, neighbors, s);
+    if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn (grid): ") + cudaGetErrorString(e));
+    cudaFree(d_pts);
+    cudaStreamDestroy(s);
+    return rc;
+  }
   const int64_t batch = std::min<int64_t>(nq, int64_t(1) << 20);
   const int64_t slots = ((batch + 127) / 128) * 128;
   rc = dalloc(&d_pts, n);

@@ -113,6 +113,11 @@ cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* 
                               int64_t q_offset, int pred, int32_t m, int64_t* d_out, double* d_keys,
                               int32_t* d_idx, cudaStream_t stream);
 
+// Predecessor kNN by index batches with a grid over the earlier points
+// (vgp_knn.cu), bit-identical to launch_knn; h_locs / h_out on the host.
+cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n, int32_t m, int64_t batch,
+                          int64_t* h_out, cudaStream_t st);
+
 // Exact maxmin ordering (vgp_maxmin.cu): order[t] for t < n, starting at
 // `first`; bbox = (x0, x1, y0, y1) of the points; at most maxmin_capacity()
 // points (one cluster holds every chunk's metadata in shared memory).

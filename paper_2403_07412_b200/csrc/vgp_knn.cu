@@ -7,6 +7,11 @@
 // owns one query and keeps only its admission threshold (the current m-th
 // key) in a register.  The sorted top-m list lives in a global scratch laid
 // out [slot][query] so the rare insertions stay coalesced across a warp.
+#include <algorithm>
+#include <cmath>
+
+#include <cub/device/device_radix_sort.cuh>
+
 #include "vgp_internal.cuh"
 
 namespace vgp {
@@ -38,11 +43,16 @@ __device__ __forceinline__ double knn_key(double4 c, double4 t) {
 // pred != 0: query q (global index q_offset + q) is ordered target i = m + q
 // (q_offset + q) and admits candidates j < i (nearest_neighbors, vg/geo.py:342).
 // pred == 0: every candidate admissible (nearest_points, vg/geo.py:357).
+// j_lo > 0 continues a search whose top-m state (cnt_in[q] entries, sorted by
+// (key, index), all indices < j_lo) is already in the scratch: candidates
+// j >= j_lo are larger than every stored index, so the ascending-j insertion
+// rule below stays exactly the lexicographic (key, index) order.
 template <typename PT>
 __global__ void __launch_bounds__(kKnnThreads)
 knn_kernel(const PT* __restrict__ data, int64_t nd, const PT* __restrict__ query,
            int64_t nq, int64_t q_offset, int pred, int m, int64_t* __restrict__ out,
-           double* __restrict__ keys, int32_t* __restrict__ idx) {
+           double* __restrict__ keys, int32_t* __restrict__ idx, int64_t j_lo,
+           const int* __restrict__ cnt_in) {
   constexpr int kTile = kKnnTile * 16 / (int)sizeof(PT);
   __shared__ PT tile[kTile];
   const int64_t q = (int64_t)blockIdx.x * kKnnThreads + threadIdx.x;
@@ -63,8 +73,12 @@ knn_kernel(const PT* __restrict__ data, int64_t nd, const PT* __restrict__ query
   int32_t* ip = idx + q;
   int cnt = 0;
   double worst = __longlong_as_double(0x7ff0000000000000ll);  // +inf until full
+  if (cnt_in && active) {
+    cnt = cnt_in[q];
+    if (cnt == m) worst = kp[(int64_t)(m - 1) * stride];
+  }
 
-  for (int64_t base = 0; base < block_limit; base += kTile) {
+  for (int64_t base = j_lo; base < block_limit; base += kTile) {
     int64_t tn = block_limit - base;
     if (tn > kTile) tn = kTile;
     __syncthreads();
@@ -101,6 +115,129 @@ knn_kernel(const PT* __restrict__ data, int64_t nd, const PT* __restrict__ query
   }
 }
 
+// ---------------------------------------------------------------- grid search
+// Exact predecessor kNN in index batches (targets [s, e)): phase 1 searches
+// a uniform grid over the points [0, s) ring by ring, keeping the m smallest
+// (key, index) pairs; phase 2 is knn_kernel over the in-batch candidates
+// [s, i).  Phase 1 stops only when the current m-th key is strictly below a
+// lower bound of every key outside the searched square: the bound is the
+// target's distance to the square's boundary minus a slack that dominates
+// the cell-assignment rounding, squared with the key's own rounding (which
+// is monotone), so no candidate that could enter the top m is skipped and
+// the result equals the brute-force scan bit for bit.
+
+struct GridDesc {
+  double x0, y0, hx, hy, ihx, ihy, slack;
+  int g;  // g x g cells
+};
+
+__device__ __forceinline__ int cell_of(double v, double v0, double ih, int g) {
+  const double f = floor((v - v0) * ih);
+  return (int)fmin(fmax(f, 0.0), (double)(g - 1));
+}
+
+__global__ void grid_cell_kernel(const double2* __restrict__ pts, int64_t s, GridDesc gd,
+                                 uint32_t* __restrict__ cell, int32_t* __restrict__ ids) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= s) return;
+  const double2 p = pts[j];
+  cell[j] = (uint32_t)(cell_of(p.y, gd.y0, gd.ihy, gd.g) * gd.g + cell_of(p.x, gd.x0, gd.ihx, gd.g));
+  ids[j] = (int32_t)j;
+}
+
+__global__ void grid_bounds_kernel(const uint32_t* __restrict__ cell_sorted, int64_t s,
+                                   int32_t* __restrict__ cstart, int32_t* __restrict__ cend) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= s) return;
+  const uint32_t c = cell_sorted[p];
+  if (p == 0 || cell_sorted[p - 1] != c) cstart[c] = (int32_t)p;
+  if (p == s - 1 || cell_sorted[p + 1] != c) cend[c] = (int32_t)(p + 1);
+}
+
+__device__ __forceinline__ bool lex_less(double k, int32_t j, double kq, int32_t jq) {
+  return k < kq || (k == kq && j < jq);
+}
+
+// query q <-> ordered target t = t0 + q; scratch [slot * stride + q]
+__global__ void __launch_bounds__(kKnnThreads)
+grid_query_kernel(const double2* __restrict__ pts, int64_t t0, int64_t nq, int m, GridDesc gd,
+                  const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
+                  const int32_t* __restrict__ cpts, double* __restrict__ keys, int32_t* __restrict__ idx,
+                  int64_t stride, int* __restrict__ cnt_out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double2 pt = pts[t0 + q];
+  const int g = gd.g;
+  const int cx = cell_of(pt.x, gd.x0, gd.ihx, g), cy = cell_of(pt.y, gd.y0, gd.ihy, g);
+  double* kp = keys + q;
+  int32_t* ip = idx + q;
+  int cnt = 0;
+  double wk = __longlong_as_double(0x7ff0000000000000ll);
+  int32_t wj = INT32_MAX;
+  const double inf = wk;
+  for (int r = 0; r <= g; ++r) {
+    if (r > 0) {
+      // searched square: cells [cx - r + 1, cx + r - 1] x [cy - r + 1, cy + r - 1]
+      const int lo_x = cx - r + 1, hi_x = cx + r - 1, lo_y = cy - r + 1, hi_y = cy + r - 1;
+      if (lo_x <= 0 && hi_x >= g - 1 && lo_y <= 0 && hi_y >= g - 1) break;  // everything searched
+      if (cnt == m) {
+        double d = inf;
+        if (lo_x > 0) d = fmin(d, __dsub_rn(pt.x, gd.x0 + lo_x * gd.hx));
+        if (hi_x < g - 1) d = fmin(d, __dsub_rn(gd.x0 + (hi_x + 1) * gd.hx, pt.x));
+        if (lo_y > 0) d = fmin(d, __dsub_rn(pt.y, gd.y0 + lo_y * gd.hy));
+        if (hi_y < g - 1) d = fmin(d, __dsub_rn(gd.y0 + (hi_y + 1) * gd.hy, pt.y));
+        d = fmax(d - gd.slack, 0.0);
+        if (wk < __dmul_rn(d, d)) break;
+      }
+    }
+    // ring r: rows cy - r and cy + r over [cx - r, cx + r], columns cx +- r over the rows between
+    for (int side = 0; side < 4; ++side) {
+      int ax, ay, dx, dy, len;
+      if (r == 0) {
+        if (side) break;
+        ax = cx; ay = cy; dx = 1; dy = 0; len = 1;
+      } else if (side == 0) { ax = cx - r; ay = cy - r; dx = 1; dy = 0; len = 2 * r + 1; }
+      else if (side == 1) { ax = cx - r; ay = cy + r; dx = 1; dy = 0; len = 2 * r + 1; }
+      else if (side == 2) { ax = cx - r; ay = cy - r + 1; dx = 0; dy = 1; len = 2 * r - 1; }
+      else { ax = cx + r; ay = cy - r + 1; dx = 0; dy = 1; len = 2 * r - 1; }
+      if ((dy == 0 && (ay < 0 || ay >= g)) || (dx == 0 && (ax < 0 || ax >= g))) continue;
+      for (int u = 0; u < len; ++u) {
+        const int ix = ax + u * dx, iy = ay + u * dy;
+        if (ix < 0 || ix >= g || iy < 0 || iy >= g) continue;
+        const int c = iy * g + ix;
+        const int b = cstart[c], e = cend[c];
+        for (int pp = b; pp < e; ++pp) {
+          const int32_t j = cpts[pp];
+          const double k = knn_key(pts[j], pt);
+          if (cnt == m && !lex_less(k, j, wk, wj)) continue;
+          int p;
+          if (cnt == m) {
+            p = m - 1;
+          } else {
+            p = cnt;
+            cnt += 1;
+          }
+          while (p > 0) {
+            const double kq = kp[(int64_t)(p - 1) * stride];
+            const int32_t jq = ip[(int64_t)(p - 1) * stride];
+            if (!lex_less(k, j, kq, jq)) break;
+            kp[(int64_t)p * stride] = kq;
+            ip[(int64_t)p * stride] = jq;
+            p -= 1;
+          }
+          kp[(int64_t)p * stride] = k;
+          ip[(int64_t)p * stride] = j;
+          if (cnt == m) {
+            wk = kp[(int64_t)(m - 1) * stride];
+            wj = ip[(int64_t)(m - 1) * stride];
+          }
+        }
+      }
+    }
+  }
+  cnt_out[q] = cnt;
+}
+
 }  // namespace
 
 cudaError_t launch_knn(const double2* d_data, int64_t nd, const double2* d_query, int64_t nq,
@@ -109,7 +246,7 @@ cudaError_t launch_knn(const double2* d_data, int64_t nd, const double2* d_query
   if (nq <= 0) return cudaSuccess;
   int64_t blocks = (nq + kKnnThreads - 1) / kKnnThreads;
   knn_kernel<double2><<<(unsigned)blocks, kKnnThreads, 0, stream>>>(d_data, nd, d_query, nq, q_offset,
-                                                                    pred, m, d_out, d_keys, d_idx);
+                                                                    pred, m, d_out, d_keys, d_idx, 0, nullptr);
   return cudaGetLastError();
 }
 
@@ -119,8 +256,104 @@ cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* 
   if (nq <= 0) return cudaSuccess;
   int64_t blocks = (nq + kKnnThreads - 1) / kKnnThreads;
   knn_kernel<double4><<<(unsigned)blocks, kKnnThreads, 0, stream>>>(d_data, nd, d_query, nq, q_offset,
-                                                                    pred, m, d_out, d_keys, d_idx);
+                                                                    pred, m, d_out, d_keys, d_idx, 0, nullptr);
   return cudaGetLastError();
+}
+
+}  // namespace vgp
+
+namespace vgp {
+
+// Predecessor kNN (Euclidean) by index batches with a grid over the earlier
+// points; bit-identical to launch_knn's brute force (see grid_query_kernel).
+// locations are the ORDERED points (host); out (n - m) x m on the host.
+cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n, int32_t m, int64_t batch,
+                          int64_t* h_out, cudaStream_t st) {
+  double x0 = h_locs[0], x1 = h_locs[0], y0 = h_locs[1], y1 = h_locs[1];
+  for (int64_t i = 0; i < n; ++i) {
+    x0 = std::min(x0, h_locs[2 * i]);
+    x1 = std::max(x1, h_locs[2 * i]);
+    y0 = std::min(y0, h_locs[2 * i + 1]);
+    y1 = std::max(y1, h_locs[2 * i + 1]);
+  }
+  const int64_t nqmax = std::min<int64_t>(batch, n - m);
+  const int64_t slots = ((nqmax + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
+  const int gmax = 4096;
+  uint32_t *cell = nullptr, *cell_s = nullptr;
+  int32_t *ids = nullptr, *ids_s = nullptr, *cs = nullptr, *ce = nullptr, *kidx = nullptr, *cnt = nullptr;
+  double* kkey = nullptr;
+  int64_t* out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, cell, cell_s, ids, ids_s, (int)n, 0, 32, st);
+  auto A = [&](void** p, size_t b) {
+    if (e == cudaSuccess) e = cudaMallocAsync(p, b ? b : 1, st);
+  };
+  A((void**)&cell, sizeof(uint32_t) * n);
+  A((void**)&cell_s, sizeof(uint32_t) * n);
+  A((void**)&ids, sizeof(int32_t) * n);
+  A((void**)&ids_s, sizeof(int32_t) * n);
+  A((void**)&cs, sizeof(int32_t) * gmax * gmax);
+  A((void**)&ce, sizeof(int32_t) * gmax * gmax);
+  A((void**)&kkey, sizeof(double) * slots * m);
+  A((void**)&kidx, sizeof(int32_t) * slots * m);
+  A((void**)&cnt, sizeof(int) * slots);
+  A((void**)&out, sizeof(int64_t) * nqmax * m);
+  A(&tmp, tmp_bytes);
+  for (int64_t s0 = m; e == cudaSuccess && s0 < n; s0 += batch) {
+    const int64_t e0 = std::min(n, s0 + batch), nq = e0 - s0;
+    // grid over [0, s0): about 3 points per cell
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t)std::sqrt((double)s0 / 3.0)));
+    GridDesc gd;
+    gd.g = g;
+    gd.x0 = x0;
+    gd.y0 = y0;
+    gd.hx = x1 > x0 ? (x1 - x0) / g : 1.0;
+    gd.hy = y1 > y0 ? (y1 - y0) / g : 1.0;
+    gd.ihx = 1.0 / gd.hx;
+    gd.ihy = 1.0 / gd.hy;
+    // dominates the cell-assignment rounding (~1e-16 of the coordinate range)
+    gd.slack = 1e-9 * std::max(gd.hx, gd.hy) + 1e-12 * std::max({std::fabs(x0), std::fabs(x1), std::fabs(y0),
+                                                                  std::fabs(y1)});
+    const int bs = 256;
+    const unsigned nb = (unsigned)((s0 + bs - 1) / bs);
+    grid_cell_kernel<<<nb, bs, 0, st>>>(d_pts, s0, gd, cell, ids);
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_s, ids, ids_s, (int)s0, 0, 32, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cs, 0, sizeof(int32_t) * g * g, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ce, 0, sizeof(int32_t) * g * g, st);
+    if (e == cudaSuccess) {
+      grid_bounds_kernel<<<nb, bs, 0, st>>>(cell_s, s0, cs, ce);
+      e = cudaGetLastError();
+    }
+    const int64_t stride = ((nq + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
+    const unsigned qb = (unsigned)(stride / kKnnThreads);
+    if (e == cudaSuccess) {
+      grid_query_kernel<<<qb, kKnnThreads, 0, st>>>(d_pts, s0, nq, m, gd, cs, ce, ids_s, kkey, kidx, stride, cnt);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      knn_kernel<double2><<<qb, kKnnThreads, 0, st>>>(d_pts, n, d_pts + s0, nq, s0 - m, 1, m, out, kkey, kidx,
+                                                      s0, cnt);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_out + (s0 - m) * m, out, sizeof(int64_t) * nq * m, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  cudaFreeAsync(cell, st);
+  cudaFreeAsync(cell_s, st);
+  cudaFreeAsync(ids, st);
+  cudaFreeAsync(ids_s, st);
+  cudaFreeAsync(cs, st);
+  cudaFreeAsync(ce, st);
+  cudaFreeAsync(kkey, st);
+  cudaFreeAsync(kidx, st);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(out, st);
+  cudaFreeAsync(tmp, st);
+  return e;
 }
 
 }  // namespace vgp

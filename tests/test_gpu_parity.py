@@ -517,3 +517,54 @@ def test_maxmin_large_is_permutation_and_monotone(vg):
     nn = vg.geo.nearest_neighbors(vg.Dataset(ordered, np.zeros(n)), 1).neighbors[:, 0]
     d = ((ordered[1:] - ordered[nn]) ** 2).sum(1)
     assert np.all(np.diff(d) <= 1e-12 * d[:-1] + 1e-300)
+
+
+# ---------------------------------------------------------------- grid-pruned kNN
+
+def _grid_knn(vg, monkeypatch, locs, m, grid):
+    monkeypatch.setenv("VGP_KNN_GRID_MIN", "0" if grid else str(1 << 40))
+    return vg.nearest_neighbors(vg.Dataset(locs, np.zeros(len(locs))), m).neighbors
+
+
+@pytest.mark.parametrize("case,m", [("uniform", 30), ("clustered_dups", 60), ("lattice", 10),
+                                    ("lattice", 45), ("collinear", 20), ("two_points_spread", 7)])
+def test_grid_knn_bit_exact(vg, oracle, monkeypatch, case, m):
+    """The index-batched grid search returns the brute-force table bit for
+    bit (ties by index included) on tie-heavy and degenerate layouts."""
+    rng = np.random.default_rng(len(case) * 7 + m)
+    if case == "uniform":
+        locs = rng.random((20000, 2))
+    elif case == "clustered_dups":
+        c = rng.random((30, 2))
+        locs = c[rng.integers(0, 30, 30000)] + 0.01 * rng.standard_normal((30000, 2))
+        dup = np.arange(0, len(locs), 7)
+        locs[dup] = locs[(dup + 3) % len(locs)]
+    elif case == "lattice":
+        g = np.arange(70, dtype=np.float64)
+        locs = np.stack(np.meshgrid(g, g, indexing="ij"), -1).reshape(-1, 2)
+        locs = locs[rng.permutation(len(locs))]
+    elif case == "collinear":
+        locs = np.stack([rng.random(8000), np.full(8000, 0.5)], -1)
+    else:
+        locs = np.concatenate([rng.random((3000, 2)) * 1e-6, 1e6 + rng.random((3000, 2))])
+        locs = locs[rng.permutation(len(locs))]
+    grid = _grid_knn(vg, monkeypatch, locs, m, True)
+    brute = _grid_knn(vg, monkeypatch, locs, m, False)
+    np.testing.assert_array_equal(grid, brute)
+    if len(locs) <= 20000:
+        np.testing.assert_array_equal(grid, oracle.knn_pred(locs, m))
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("knn_") if "sphere" not in n and "points" not in n])
+def test_grid_knn_vs_reference_golden(vg, monkeypatch, name):
+    z = load(name)
+    monkeypatch.setenv("VGP_KNN_GRID_MIN", "0")
+    t = vg.nearest_neighbors(vg.Dataset(z["locs"], np.zeros(len(z["locs"]))), int(z["m"])).neighbors
+    np.testing.assert_array_equal(t, z["table"])
+
+
+def test_grid_knn_large_matches_brute_force(vg, monkeypatch):
+    rng = np.random.default_rng(77)
+    locs = rng.random((500_000, 2))
+    np.testing.assert_array_equal(_grid_knn(vg, monkeypatch, locs, 60, True),
+                                  _grid_knn(vg, monkeypatch, locs, 60, False))
