@@ -420,7 +420,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    # VGP_BENCH_FORCE_MULTI=1 runs the sharded NCCL path even at world size 1
+    # (how the multi-GPU code path is exercised on a one-GPU box)
+    if world > 1 or os.environ.get("VGP_BENCH_FORCE_MULTI") == "1":
         run_ours_multi(args, rank, world)
     else:
         run_ours_single(args)
