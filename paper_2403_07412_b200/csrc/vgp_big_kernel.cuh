@@ -52,7 +52,14 @@ constexpr int kHead = 256 + 64 + 8 + 5 * kBesselTab;  // exp table | Lt | Iv | B
 
 __host__ __device__ inline int ntiles_of(int m) { return (m + 2 + 7) / 8; }
 // doubles of the shared-memory area besides the tiles
-__host__ __device__ inline int head_doubles(int m) { return kHead + 3 * 8 * ntiles_of(m) + 4; }
+// the Bessel tables only exist for general nu: the closed forms keep 2.5 KB
+// more shared memory per CTA (m = 120: 75.4 KB, 3 CTAs per SM instead of 2)
+__host__ __device__ constexpr int head_fixed(int kind) {
+  return 256 + 64 + 8 + (kind == kMaternGen ? 5 * kBesselTab : 0);
+}
+__host__ __device__ inline int head_doubles(int m, int kind = kMaternGen) {
+  return head_fixed(kind) + 3 * 8 * ntiles_of(m) + 4;
+}
 __host__ __device__ inline int64_t tile_doubles(int m) {
   const int nt = ntiles_of(m);
   return (int64_t)ntri(nt) * 64;
@@ -81,7 +88,7 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
 }
 
 template <int KIND, bool CACHE, bool GT>
-__global__ void __launch_bounds__(kThreads, KIND == kMaternGen ? 4 : 1)
+__global__ void __launch_bounds__(kThreads, 4)
 loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
                   int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
@@ -96,10 +103,10 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   double* Lt = smem + 256;  // L_cc transposed: Lt[8k + j] = L[j][k]
   double* Iv = Lt + 64;     // reciprocal pivots
   double* Bt = Iv + 8;      // general-nu Bessel reciprocal tables
-  double* O = smem + kHead;  // yJ row (row m+1)
+  double* O = smem + head_fixed(KIND);  // yJ row (row m+1)
   double2* XY = reinterpret_cast<double2*>(O + P);
   double* Y = O + 3 * P;  // target observation
-  double* T = GT ? gscratch + (size_t)blockIdx.x * tile_doubles(m) : smem + head_doubles(m);
+  double* T = GT ? gscratch + (size_t)blockIdx.x * tile_doubles(m) : smem + head_doubles(m, KIND);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2;  // fragment row
@@ -354,8 +361,8 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   }
 }
 
-inline size_t smem_bytes(int m, bool gt) {
-  return sizeof(double) * ((size_t)head_doubles(m) + (gt ? 0 : (size_t)tile_doubles(m)));
+inline size_t smem_bytes(int m, bool gt, int kind = kMaternGen) {
+  return sizeof(double) * ((size_t)head_doubles(m, kind) + (gt ? 0 : (size_t)tile_doubles(m)));
 }
 // tiles in shared memory up to ~200 KB per CTA, else the global scratch
 inline bool use_global_tiles(int m) { return smem_bytes(m, false) > 200 * 1024; }
@@ -363,7 +370,7 @@ inline bool use_global_tiles(int m) { return smem_bytes(m, false) > 200 * 1024; 
 template <int KIND, bool CACHE, bool GT>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, double* gscratch, int max_grid) {
-  const size_t sm = smem_bytes(p.m, GT);
+  const size_t sm = smem_bytes(p.m, GT, KIND);
   auto kern = loglik_big_kernel<KIND, CACHE, GT>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (err != cudaSuccess) return err;
