@@ -236,12 +236,14 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     // for general nu / power exponential, where covariance generation
     // dominates, streaming them is 1.6x faster, profiles/r01_c5_general_nu.txt)
     const bool big_prefer_cache = cp.kind >= kMaternGen;
-    // small blocks (m + 2 <= 32): one warp per block with everything in
-    // registers beats warp specialisation (profiles/r01_smallm_variants.txt)
-    const bool small = p->m + 2 <= 32;
+    // by tile count (profiles/r01_smallm_variants.txt): up to 3 tile columns
+    // one warp per block with everything in registers wins; up to 7 the
+    // warp-specialised pair streaming the cache; 8 the scheduler-aware layout
+    const bool small = p->m + 2 <= 24;
+    const bool mid = p->m + 2 <= 56;
     if (v < 0)
       v = small && fast_n ? 1
-        : small && fast_c ? 4
+        : (small || mid) && fast_c ? 4
         : fast_c ? 8
         : (fast_n ? 7
                   : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));

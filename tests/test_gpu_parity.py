@@ -121,8 +121,8 @@ def test_loglik_vs_reference_golden(vg, name, variant):
     # the cache exists for m + 2 <= 64 and for great-circle plans; the large-m
     # kernel computes Euclidean distances for the closed forms and streams
     # the cache for general nu / power exponential when there is one
-    small = int(z["m"]) + 2 <= 32
-    auto = ((1 if plane else 4) if small else 8) if fast else (
+    small, mid = int(z["m"]) + 2 <= 24, int(z["m"]) + 2 <= 56
+    auto = ((1 if plane else 4) if small else (4 if mid else 8)) if fast else (
         12 if cache and (not plane or not closed) else 11)
     assert plan.device_plan().kernel_variant == (variant if variant >= 0 else auto)
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL

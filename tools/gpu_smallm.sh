@@ -1,6 +1,6 @@
 #!/bin/bash
 # small-m regime: every kernel variant at n = 250k
-for m in 10 20 30; do for v in 0 1 2 3 4 7 8 11 12; do
+for m in ${MS:-10 20 30}; do for v in ${VS:-0 1 2 3 4 7 8 11 12}; do
   timeout 300 python bench.py --n 250000 --m $m --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline --variant $v 2>&1 | tail -1 | python -c "
 import json,sys
 try:
