@@ -515,6 +515,20 @@ int vgp_knn_sphere(int device, const double* data3, int64_t nd, const double* qu
     hq[i] = make_double4(query3[3 * i], query3[3 * i + 1], query3[3 * i + 2], 0.0);
   cudaStream_t s;
   VGP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int64_t grid_min = 200000;  // as vgp_knn_predecessors
+  if (const char* env = std::getenv("VGP_KNN_GRID_MIN")) grid_min = std::atoll(env);
+  if (predecessors && nd >= grid_min) {
+    double4* d_pts = nullptr;
+    rc = dalloc(&d_pts, nd);
+    cudaError_t e = cudaSuccess;
+    if (!rc) e = cudaMemcpyAsync(d_pts, hd.data(), sizeof(double4) * nd, cudaMemcpyHostToDevice, s);
+    if (!rc && e == cudaSuccess) e = knn_pred_grid_sphere(d_pts, nd, m, 32768, neighbors, s);
+    if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn sphere (grid): ") + cudaGetErrorString(e));
+    cudaFree(d_pts);
+    cudaStreamDestroy(s);
+    return rc;
+  }
   double4 *d_data = nullptr, *d_q = nullptr;
   int64_t* d_out = nullptr;
   double* d_keys = nullptr;

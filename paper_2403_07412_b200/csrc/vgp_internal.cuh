@@ -118,6 +118,10 @@ cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* 
 cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n, int32_t m, int64_t batch,
                           int64_t* h_out, cudaStream_t st);
 
+// The same for great-circle plans: points (lambda, phi, cos phi, 0) on the device.
+cudaError_t knn_pred_grid_sphere(const double4* d_pts, int64_t n, int32_t m, int64_t batch, int64_t* h_out,
+                                 cudaStream_t st);
+
 // Exact maxmin ordering (vgp_maxmin.cu): order[t] for t < n, starting at
 // `first`; bbox = (x0, x1, y0, y1) of the points; at most maxmin_capacity()
 // points (one cluster holds every chunk's metadata in shared memory).

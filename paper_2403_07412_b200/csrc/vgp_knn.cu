@@ -357,3 +357,198 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
 }
 
 }  // namespace vgp
+
+// ---------------------------------------------------------------- sphere grid
+// Great-circle predecessor kNN by index batches.  Points (lambda, phi,
+// cos phi) map to unit vectors; the haversine key equals chord^2 / 4 in exact
+// arithmetic, so a cube grid over [-1, 1]^3 gives a lower bound for every
+// point outside the searched cube: (distance to the cube's faces, minus an
+// absolute slack)^2 / 4, shrunk by a relative slack far above the key's few-
+// ulp error (sin) and the unit vectors' rounding.  Shells are searched until
+// the m-th key is strictly below that bound; the in-batch candidates then go
+// through the sphere brute-force kernel as in the plane case.
+
+namespace vgp {
+namespace {
+
+__global__ void sph_unit_kernel(const double4* __restrict__ pts, int64_t n, double4* __restrict__ u) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double4 p = pts[j];  // (lambda, phi, cos phi)
+  double sl, cl;
+  sincos(p.x, &sl, &cl);
+  u[j] = make_double4(p.z * cl, p.z * sl, sin(p.y), 0.0);
+}
+
+__device__ __forceinline__ int cell3(double v, double ih, int g) {
+  const double f = floor((v + 1.0) * ih);
+  return (int)fmin(fmax(f, 0.0), (double)(g - 1));
+}
+
+__global__ void grid3_cell_kernel(const double4* __restrict__ u, int64_t s, int g, double ih,
+                                  uint32_t* __restrict__ cell, int32_t* __restrict__ ids) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= s) return;
+  const double4 p = u[j];
+  cell[j] = (uint32_t)(((int64_t)cell3(p.z, ih, g) * g + cell3(p.y, ih, g)) * g + cell3(p.x, ih, g));
+  ids[j] = (int32_t)j;
+}
+
+__global__ void __launch_bounds__(kKnnThreads)
+grid3_query_kernel(const double4* __restrict__ pts, const double4* __restrict__ u, int64_t t0, int64_t nq, int m,
+                   int g, double h, double ih, const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
+                   const int32_t* __restrict__ cpts, double* __restrict__ keys, int32_t* __restrict__ idx,
+                   int64_t stride, int* __restrict__ cnt_out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double4 pt = pts[t0 + q];
+  const double4 ut = u[t0 + q];
+  const int c[3] = {cell3(ut.x, ih, g), cell3(ut.y, ih, g), cell3(ut.z, ih, g)};
+  const double tc[3] = {ut.x, ut.y, ut.z};
+  double* kp = keys + q;
+  int32_t* ip = idx + q;
+  int cnt = 0;
+  double wk = __longlong_as_double(0x7ff0000000000000ll);
+  int32_t wj = INT32_MAX;
+  for (int r = 0; r <= g; ++r) {
+    if (r > 0) {
+      bool all = true;
+      double d = __longlong_as_double(0x7ff0000000000000ll);
+      for (int a = 0; a < 3; ++a) {
+        const int lo = c[a] - r + 1, hi = c[a] + r - 1;
+        if (lo > 0) {
+          all = false;
+          d = fmin(d, tc[a] - (-1.0 + lo * h));
+        }
+        if (hi < g - 1) {
+          all = false;
+          d = fmin(d, (-1.0 + (hi + 1) * h) - tc[a]);
+        }
+      }
+      if (all) break;  // the whole cube searched
+      if (cnt == m) {
+        d = fmax(d - 1e-9 * h, 0.0);
+        if (wk < d * d * 0.25 * (1.0 - 1e-9)) break;
+      }
+    }
+    for (int dz = -r; dz <= r; ++dz) {
+      const int iz = c[2] + dz;
+      if (iz < 0 || iz >= g) continue;
+      for (int dy = -r; dy <= r; ++dy) {
+        const int iy = c[1] + dy;
+        if (iy < 0 || iy >= g) continue;
+        const bool face = (dz == -r || dz == r || dy == -r || dy == r);
+        for (int dx = -r; dx <= r; dx += (face || r == 0) ? 1 : 2 * r) {
+          const int ix = c[0] + dx;
+          if (ix < 0 || ix >= g) continue;
+          const int64_t cc = ((int64_t)iz * g + iy) * g + ix;
+          const int b = cstart[cc], e = cend[cc];
+          for (int pp = b; pp < e; ++pp) {
+            const int32_t j = cpts[pp];
+            const double k = knn_key(pts[j], pt);
+            if (cnt == m && !lex_less(k, j, wk, wj)) continue;
+            int p;
+            if (cnt == m) {
+              p = m - 1;
+            } else {
+              p = cnt;
+              cnt += 1;
+            }
+            while (p > 0) {
+              const double kq = kp[(int64_t)(p - 1) * stride];
+              const int32_t jq = ip[(int64_t)(p - 1) * stride];
+              if (!lex_less(k, j, kq, jq)) break;
+              kp[(int64_t)p * stride] = kq;
+              ip[(int64_t)p * stride] = jq;
+              p -= 1;
+            }
+            kp[(int64_t)p * stride] = k;
+            ip[(int64_t)p * stride] = j;
+            if (cnt == m) {
+              wk = kp[(int64_t)(m - 1) * stride];
+              wj = ip[(int64_t)(m - 1) * stride];
+            }
+          }
+        }
+      }
+    }
+  }
+  cnt_out[q] = cnt;
+}
+
+}  // namespace
+
+cudaError_t knn_pred_grid_sphere(const double4* d_pts, int64_t n, int32_t m, int64_t batch, int64_t* h_out,
+                                 cudaStream_t st) {
+  const int64_t nqmax = std::min<int64_t>(batch, n - m);
+  const int64_t slots = ((nqmax + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
+  const int gmax = 320;
+  const int64_t ncell_max = (int64_t)gmax * gmax * gmax;
+  uint32_t *cell = nullptr, *cell_s = nullptr;
+  int32_t *ids = nullptr, *ids_s = nullptr, *cs = nullptr, *ce = nullptr, *kidx = nullptr, *cnt = nullptr;
+  double* kkey = nullptr;
+  double4* u = nullptr;
+  int64_t* out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, cell, cell_s, ids, ids_s, (int)n, 0, 32, st);
+  auto A = [&](void** p, size_t b) {
+    if (e == cudaSuccess) e = cudaMallocAsync(p, b ? b : 1, st);
+  };
+  A((void**)&u, sizeof(double4) * n);
+  A((void**)&cell, sizeof(uint32_t) * n);
+  A((void**)&cell_s, sizeof(uint32_t) * n);
+  A((void**)&ids, sizeof(int32_t) * n);
+  A((void**)&ids_s, sizeof(int32_t) * n);
+  A((void**)&cs, sizeof(int32_t) * ncell_max);
+  A((void**)&ce, sizeof(int32_t) * ncell_max);
+  A((void**)&kkey, sizeof(double) * slots * m);
+  A((void**)&kidx, sizeof(int32_t) * slots * m);
+  A((void**)&cnt, sizeof(int) * slots);
+  A((void**)&out, sizeof(int64_t) * nqmax * m);
+  A(&tmp, tmp_bytes);
+  const int bs = 256;
+  if (e == cudaSuccess) {
+    sph_unit_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(d_pts, n, u);
+    e = cudaGetLastError();
+  }
+  for (int64_t s0 = m; e == cudaSuccess && s0 < n; s0 += batch) {
+    const int64_t e0 = std::min(n, s0 + batch), nq = e0 - s0;
+    // ~3 points per occupied cell: about 4.7 g^2 cells meet the sphere
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t)std::sqrt((double)s0 / 14.0)));
+    const double h = 2.0 / g, ih = g / 2.0;
+    const int64_t ncell = (int64_t)g * g * g;
+    const unsigned nb = (unsigned)((s0 + bs - 1) / bs);
+    grid3_cell_kernel<<<nb, bs, 0, st>>>(u, s0, g, ih, cell, ids);
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_s, ids, ids_s, (int)s0, 0, 32, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cs, 0, sizeof(int32_t) * ncell, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ce, 0, sizeof(int32_t) * ncell, st);
+    if (e == cudaSuccess) {
+      grid_bounds_kernel<<<nb, bs, 0, st>>>(cell_s, s0, cs, ce);
+      e = cudaGetLastError();
+    }
+    const int64_t stride = ((nq + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
+    const unsigned qb = (unsigned)(stride / kKnnThreads);
+    if (e == cudaSuccess) {
+      grid3_query_kernel<<<qb, kKnnThreads, 0, st>>>(d_pts, u, s0, nq, m, g, h, ih, cs, ce, ids_s, kkey, kidx,
+                                                     stride, cnt);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      knn_kernel<double4><<<qb, kKnnThreads, 0, st>>>(d_pts, n, d_pts + s0, nq, s0 - m, 1, m, out, kkey, kidx,
+                                                      s0, cnt);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_out + (s0 - m) * m, out, sizeof(int64_t) * nq * m, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  for (void* p : {(void*)u, (void*)cell, (void*)cell_s, (void*)ids, (void*)ids_s, (void*)cs, (void*)ce,
+                  (void*)kkey, (void*)kidx, (void*)cnt, (void*)out, tmp})
+    cudaFreeAsync(p, st);
+  return e;
+}
+
+}  // namespace vgp

@@ -568,3 +568,51 @@ def test_grid_knn_large_matches_brute_force(vg, monkeypatch):
     locs = rng.random((500_000, 2))
     np.testing.assert_array_equal(_grid_knn(vg, monkeypatch, locs, 60, True),
                                   _grid_knn(vg, monkeypatch, locs, 60, False))
+
+
+@pytest.mark.parametrize("case,m", [("global", 30), ("polar", 20), ("dateline", 12), ("dups", 40)])
+def test_sphere_grid_knn_bit_exact(vg, monkeypatch, case, m):
+    """Great-circle grid search (unit-vector cube grid, chord bound) equals
+    the sphere brute-force kernel bit for bit."""
+    rng = np.random.default_rng(len(case) + m)
+    n = 30000
+    if case == "global":
+        lon, lat = rng.uniform(-180, 180, n), np.degrees(np.arcsin(rng.uniform(-1, 1, n)))
+    elif case == "polar":
+        lon, lat = rng.uniform(-180, 180, n), rng.uniform(88.0, 90.0, n)
+    elif case == "dateline":
+        lon = np.where(rng.random(n) < 0.5, rng.uniform(179.0, 180.0, n), rng.uniform(-180.0, -179.0, n))
+        lat = rng.uniform(-5, 5, n)
+    else:
+        lon, lat = rng.uniform(-20, 20, n), rng.uniform(30, 50, n)
+        dup = np.arange(0, n, 5)
+        lon[dup], lat[dup] = lon[(dup + 2) % n], lat[(dup + 2) % n]
+    locs = np.stack([lon, lat], -1)
+    gc = vg.GreatCircle()
+
+    def table(grid):
+        monkeypatch.setenv("VGP_KNN_GRID_MIN", "0" if grid else str(1 << 40))
+        return vg.nearest_neighbors(vg.Dataset(locs, np.zeros(n), gc), m).neighbors
+
+    np.testing.assert_array_equal(table(True), table(False))
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("knn_sphere") if "points" not in n])
+def test_sphere_grid_knn_vs_reference_golden(vg, monkeypatch, name):
+    z = load(name)
+    monkeypatch.setenv("VGP_KNN_GRID_MIN", "0")
+    t = vg.nearest_neighbors(vg.Dataset(z["locs"], np.zeros(len(z["locs"])), vg.GreatCircle()),
+                             int(z["m"])).neighbors
+    np.testing.assert_array_equal(t, z["table"])
+
+
+def test_sphere_grid_knn_large(vg, monkeypatch):
+    rng = np.random.default_rng(123)
+    n = 300_000
+    locs = np.stack([rng.uniform(-180, 180, n), np.degrees(np.arcsin(rng.uniform(-1, 1, n)))], -1)
+    gc = vg.GreatCircle()
+    out = []
+    for grid in (True, False):
+        monkeypatch.setenv("VGP_KNN_GRID_MIN", "0" if grid else str(1 << 40))
+        out.append(vg.nearest_neighbors(vg.Dataset(locs, np.zeros(n), gc), 30).neighbors)
+    np.testing.assert_array_equal(out[0], out[1])
