@@ -315,7 +315,7 @@ def run_ours_single(args):
         "gpu_launches": KERNELS_PER_EVAL * args.steps,
         "clocks": clk.summary(),
         "plan_s": round(knn_s, 3), "total": total,
-        "kernel_variant": {0: "generic", 1: "warp-dmma-allreg", 2: "warp-dmma-grouped", 3: "warp-specialised", 4: "warp-specialised+dcache", 5: "ws-short-chain", 6: "ws-short-chain+dcache", 7: "ws-scheduler-aware", 8: "ws-scheduler-aware+dcache", 9: "ws-chain-isolated", 10: "ws-chain-isolated+dcache", 11: "large-m-cta", 12: "large-m-cta+dcache"}.get(dp.kernel_variant, "?"),
+        "kernel_variant": {0: "generic", 1: "warp-dmma-allreg", 2: "warp-dmma-grouped", 3: "warp-specialised", 4: "warp-specialised+dcache", 5: "ws-short-chain", 6: "ws-short-chain+dcache", 7: "ws-scheduler-aware", 8: "ws-scheduler-aware+dcache", 9: "ws-chain-isolated", 10: "ws-chain-isolated+dcache", 11: "large-m-cta", 12: "large-m-cta+dcache", 13: "thread-per-block"}.get(dp.kernel_variant, "?"),
     }
     if not args.no_cpu_baseline:
         ordered = data.permute(plan.permutation)

@@ -205,14 +205,16 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches);
  * [8] = distance cache valid.  info must hold 9 entries. */
 int vgp_plan_info(const vgp_plan* plan, int64_t* info);
 
-/* Force a kernel variant — testing / benchmarking aid.  -1 auto (8 when the
- * plan has a distance cache, else 7, for m + 2 <= 64 closed-form Matern and
- * the Euclidean metric; 12 / 11 for larger m; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
+/* Force a kernel variant — testing / benchmarking aid.  -1 auto (by m, for
+ * closed-form Matern: 13 for m <= 10 (Euclidean), 1 for m + 2 <= 24, 4 for
+ * m + 2 <= 56, 8 for m + 2 <= 64 — cached variants when the plan has a
+ * distance cache; 11 / 12 for larger m and for general nu / power
+ * exponential; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
  * 2 grouped warp-DMMA, 3/4 warp-specialised, 7/8 scheduler-aware
- * warp-specialised (default; 5, 6, 9, 10 are retired experiments returning
- * VGP_E_CUDA), 11/12 the CTA-per-block large-m
- * DMMA kernel (any m, auto for m + 2 > 64 closed-form Matern); even numbers
- * >= 4 stream the plan's distance cache. */
+ * warp-specialised (5, 6, 9, 10 are retired experiments returning
+ * VGP_E_UNSUPPORTED), 11/12 the CTA-per-block large-m DMMA kernel (any m,
+ * every family), 13 thread-per-block (m <= 10, closed-form Matern,
+ * Euclidean); even numbers 4..12 stream the plan's distance cache. */
 int vgp_plan_set_variant(vgp_plan* plan, int variant);
 
 /* CUDA stream (cudaStream_t) the plan launches on, for event timing. */

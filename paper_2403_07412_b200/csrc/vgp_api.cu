@@ -241,14 +241,17 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     // warp-specialised pair streaming the cache; 8 the scheduler-aware layout
     const bool small = p->m + 2 <= 24;
     const bool mid = p->m + 2 <= 56;
+    const bool tiny = tiny_supported(p->m, cp.kind) && eu;
     if (v < 0)
-      v = small && fast_n ? 1
+      v = tiny ? 13
+        : small && fast_n ? 1
         : (small || mid) && fast_c ? 4
         : fast_c ? 8
         : (fast_n ? 7
                   : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
     const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
-                    ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c);
+                    ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c) ||
+                    (v == 13 && tiny);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
@@ -264,6 +267,7 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
       if (v <= 4) return launch_loglik_ws(*p, cp, lo, hi, s, v == 4);
       if (v <= 6 || v >= 9 && v <= 10) return cudaErrorNotSupported;  // retired variants
       if (v <= 8) return launch_loglik_ws3(*p, cp, lo, hi, s, v == 8);
+      if (v == 13) return launch_loglik_tiny(*p, cp, lo, hi, s);
       return launch_loglik_big(*p, cp, lo, hi, s, v == 12);
     };
     const int64_t count = e_hi - e_lo;
@@ -1033,7 +1037,7 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 12) return fail(VGP_E_INVALID, "bad variant");
+  if (!plan || variant < -1 || variant > 13) return fail(VGP_E_INVALID, "bad variant");
   // -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
   // 3 warp-specialised DMMA, 4 warp-specialised streaming the distance cache
   plan->p.force_variant = variant;

@@ -122,6 +122,11 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
 cudaError_t knn_pred_grid_sphere(const double4* d_pts, int64_t n, int32_t m, int64_t batch, int64_t* h_out,
                                  cudaStream_t st);
 
+// Thread-per-block kernel for m <= 10, closed-form Matern, Euclidean (vgp_tiny.cu).
+bool tiny_supported(int m, int kind);
+cudaError_t launch_loglik_tiny(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                               cudaStream_t stream);
+
 // Exact maxmin ordering (vgp_maxmin.cu): order[t] for t < n, starting at
 // `first`; bbox = (x0, x1, y0, y1) of the points; at most maxmin_capacity()
 // points (one cluster holds every chunk's metadata in shared memory).

@@ -102,7 +102,7 @@ def _plan_from_golden(vg, z):
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
-@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 7, 8, 11, 12])
+@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 7, 8, 11, 12, 13])
 def test_loglik_vs_reference_golden(vg, name, variant):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
@@ -116,13 +116,16 @@ def test_loglik_vs_reference_golden(vg, name, variant):
     cache = not plane or int(z["m"]) + 2 <= 64
     if variant == 12 and not cache:
         pytest.skip("large-m Euclidean plans carry no distance cache")
+    tiny = closed and plane and int(z["m"]) <= 10
+    if variant == 13 and not tiny:
+        pytest.skip("thread-per-block kernel: m <= 10, closed-form Matern, Euclidean")
     plan.device_plan().set_variant(variant)
     res = vg.vecchia_loglik(data, plan, spec)
     # the cache exists for m + 2 <= 64 and for great-circle plans; the large-m
     # kernel computes Euclidean distances for the closed forms and streams
     # the cache for general nu / power exponential when there is one
     small, mid = int(z["m"]) + 2 <= 24, int(z["m"]) + 2 <= 56
-    auto = ((1 if plane else 4) if small else (4 if mid else 8)) if fast else (
+    auto = 13 if tiny else ((1 if plane else 4) if small else (4 if mid else 8)) if fast else (
         12 if cache and (not plane or not closed) else 11)
     assert plan.device_plan().kernel_variant == (variant if variant >= 0 else auto)
     assert rel(res.total, float(z["total"])) <= TOL_TOTAL
