@@ -206,14 +206,14 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches);
 int vgp_plan_info(const vgp_plan* plan, int64_t* info);
 
 /* Force a kernel variant — testing / benchmarking aid.  -1 auto (by m, for
- * closed-form Matern: 13 for m <= 10 (Euclidean), 1 for m + 2 <= 24, 4 for
+ * closed-form Matern: 13 for m <= 12 (Euclidean), 1 for m + 2 <= 24, 4 for
  * m + 2 <= 56, 8 for m + 2 <= 64 — cached variants when the plan has a
  * distance cache; 11 / 12 for larger m and for general nu / power
  * exponential; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
  * 2 grouped warp-DMMA, 3/4 warp-specialised, 7/8 scheduler-aware
  * warp-specialised (5, 6, 9, 10 are retired experiments returning
  * VGP_E_UNSUPPORTED), 11/12 the CTA-per-block large-m DMMA kernel (any m,
- * every family), 13 thread-per-block (m <= 10, closed-form Matern,
+ * every family), 13 thread-per-block (m <= 12, closed-form Matern,
  * Euclidean); even numbers 4..12 stream the plan's distance cache. */
 int vgp_plan_set_variant(vgp_plan* plan, int variant);
 

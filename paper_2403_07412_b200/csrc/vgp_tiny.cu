@@ -1,4 +1,4 @@
-// Thread-per-block kernel for small conditioning sets (m <= 10), variant 13.
+// Thread-per-block kernel for small conditioning sets (m <= 12), variant 13.
 //
 // At small m a block is a few hundred flops, and the warp-per-block DMMA
 // kernels spend ~1,300 issue cycles per block on 8x8-tile bookkeeping and
@@ -19,7 +19,7 @@ namespace vgp {
 namespace tiny {
 
 constexpr int kThreads = 128;
-constexpr int kMaxM = 10;
+constexpr int kMaxM = 12;  // m = 11, 12 spill a few bytes at 254 registers and still run 3x the warp kernel
 
 template <int M>
 struct Tri {
@@ -131,6 +131,8 @@ cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_
     case 8: return launch_m<8, KIND>(p, cp, e_lo, e_hi, s);
     case 9: return launch_m<9, KIND>(p, cp, e_lo, e_hi, s);
     case 10: return launch_m<10, KIND>(p, cp, e_lo, e_hi, s);
+    case 11: return launch_m<11, KIND>(p, cp, e_lo, e_hi, s);
+    case 12: return launch_m<12, KIND>(p, cp, e_lo, e_hi, s);
     default: return cudaErrorNotSupported;
   }
 }
