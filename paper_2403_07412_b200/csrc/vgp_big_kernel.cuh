@@ -88,7 +88,7 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
 }
 
 template <int KIND, bool CACHE, bool GT>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, GT ? 3 : 4)
 loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
                   int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
