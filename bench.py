@@ -36,8 +36,28 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-FP64_PEAK_TFLOPS = 37.0  # measured DMMA m8n8k4 peak on this pool's B200 (profiles/r01_fp64_peak.jsonl)
-FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA.8x8x4, 148 SMs @1965 MHz (profiles/r01_fp64_peak.jsonl)"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.jsonl")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def fp64_peak():
+    """Builder-measured FP64 peak (DMMA.8x8x4 stream on all 148 SMs; MEASURED_PEAKS.json
+    carries no FP64 figure): the best dmma_m8n8k4 line of profiles/r01_fp64_peak.jsonl."""
+    best = None
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            for line in f:
+                rec = json.loads(line)
+                if rec.get("kernel") == "dmma_m8n8k4":
+                    best = max(best or 0.0, float(rec["tflops"]))
+    except OSError:
+        pass
+    if best is None:
+        return 37.0, "fallback 37.0 TFLOP/s (profiles/r01_fp64_peak.jsonl missing)"
+    return best, ("of builder-measured DMMA peak: tools/fp64_peak.cu DMMA.8x8x4 stream, "
+                  "148 SMs @1965 MHz (profiles/r01_fp64_peak.jsonl)")
+
+
 KERNELS_PER_EVAL = 4  # joint block, fused block kernel, chunk partials, ordered total
 
 
@@ -65,6 +85,7 @@ def parse():
 
 
 def synthetic(n, seed=0, kind="uniform"):
+    """Locations of the workload (observations come from simulate_vecchia)."""
     rng = np.random.default_rng(seed)
     if kind == "clustered":
         # 200 Gaussian clusters (sd 0.02) holding 80% of the points, 20% uniform
@@ -74,9 +95,19 @@ def synthetic(n, seed=0, kind="uniform"):
                                rng.random((n - k, 2))])
     else:
         locs = rng.random((n, 2))
-    # timing only needs a finite field (as the reference's own bench, vg/cli.py:245-250)
-    y = rng.standard_normal(n)
-    return locs, y
+    return locs
+
+
+Y_SEED = 1  # z ~ N(0, I) of the Vecchia forward simulation
+
+
+def simulated_dataset(vg, locs, plan, args):
+    """Observations drawn from the Vecchia model of the plan at the evaluation
+    parameters (model-consistent y keeps the 1e-9 CPU/GPU gate
+    meaningful; white noise does not).  Runs on the GPU (vgp_simulate)."""
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, args.beta, args.nu))
+    y = vg.simulate_vecchia(vg.Dataset(locs, np.zeros(locs.shape[0])), plan, spec, Y_SEED)
+    return vg.Dataset(locs, y)
 
 
 def workload(args):
@@ -86,7 +117,9 @@ def workload(args):
                 "morton": "morton"}[args.ordering]
     return {"workload": "vecchia_loglik", "n": args.n, "m": args.m, "kernel": "matern",
             "nu": args.nu, "sigma_sq": 1.0, "beta": args.beta, "ordering": ordering,
-            "locations": locs, "l2": "inputs > L2 (272 MB), no flush"}
+            "locations": locs, "observations": f"Vecchia forward simulation at the evaluation "
+            f"parameters (vgp_simulate, z seed {Y_SEED})",
+            "l2": "inputs > L2 (272 MB), no flush"}
 
 
 def flop_count(n, m):
@@ -152,39 +185,106 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU baseline
 
-def cpu_baseline(args, locs_ordered, y_ordered, table, threads=None):
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+PORT_NOTE = ("oracle/vecchia_oracle.c: the reference algorithm restated in C (fixed-chunk "
+             "threads like vg/parallel.py); its POTRF updates the lower triangle only where "
+             "the reference's _potrf_sweep updates the full trailing block "
+             "(vg/batchla.py:146-156), so it is faster than the reference's own code "
+             "(94.6 s/eval on 8 cores, SURVEY.md §3.1)")
+
+
+def cpu_baseline(args, ordered, table, gpu_res):
     """Oracle C restatement (oracle/vecchia_oracle.c) on a prefix of the same
     ordered problem: the first n' ordered points form exactly the first
-    n' - m + 1 blocks.  Returns (evals/s extrapolated, sample description,
-    seconds, threads)."""
+    n' - m + 1 blocks.  Also the parity check of the run: the oracle's total
+    on that prefix against the GPU's per-block results over the same blocks,
+    and the oracle's neighbour table on a prefix against the GPU's."""
+    import hashlib
+
     from oracle import oracle as O
 
-    threads = threads or (os.cpu_count() or 1)
+    import paper_2403_07412_b200 as vg
+
+    threads = os.cpu_count() or 1
     m = args.m
+    locs, obs = ordered.locations, ordered.observations
+    closed = args.nu in (0.5, 1.5, 2.5)
 
     def run(nn):
         t0 = time.perf_counter()
-        r = O.loglik(locs_ordered[:nn], y_ordered[:nn], m, table[: nn - m], "matern", 1.0,
-                     args.beta, args.nu, threads=threads)
+        r = O.loglik(locs[:nn], obs[:nn], m, table[: nn - m], "matern", 1.0, args.beta,
+                     args.nu, threads=threads)
         dt = time.perf_counter() - t0
         if r.status != 0:
             raise RuntimeError(f"oracle evaluation failed: status {r.status}")
-        return dt
+        return r, dt
 
-    n_cal = min(args.n, 20000)
-    t_cal = run(n_cal)
-    blocks_cal = n_cal - m + 1
-    per_block = t_cal / blocks_cal
+    n_cal = min(args.n, 20000 if closed else 3000)
+    r, t_cal = run(n_cal)
+    per_block = t_cal / (n_cal - m + 1)
     n_s = int(min(args.n, max(n_cal, args.cpu_seconds / per_block + m - 1)))
-    t_s = run(n_s) if n_s > n_cal else t_cal
+    if n_s > n_cal:
+        r, t_s = run(n_s)
+    else:
+        t_s = t_cal
     blocks_s = n_s - m + 1
     sec_per_eval = t_s / blocks_s * (args.n - m + 1)
     sample = (f"prefix n'={n_s} of the ordered problem ({blocks_s} of {args.n - m + 1} blocks, "
               f"{t_s:.1f}s), extrapolated per block")
-    return 1.0 / sec_per_eval, sample, t_s, threads
+    # parity over the same blocks: total == block_first + _ordered_sum(block_rest)
+    k = n_s - m
+    gpu_prefix = gpu_res.block_first + vg.vecchia._ordered_sum(gpu_res.block_rest[:k])
+    rest_rel = np.abs(gpu_res.block_rest[:k] - r.block_rest) / np.maximum(np.abs(r.block_rest), 1e-300)
+    n_knn = int(min(args.n, 200000))
+    t0 = time.perf_counter()
+    knn_ref = O.knn_pred(locs[:n_knn], m, threads)
+    knn_s = time.perf_counter() - t0
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+    parity = {
+        "rel_err": abs(gpu_prefix - r.total) / abs(r.total),
+        "blocks": blocks_s, "of_blocks": args.n - m + 1,
+        "gpu_total": gpu_prefix, "oracle_total": r.total,
+        "block_rest_max_rel_err": float(rest_rel.max()) if k else 0.0,
+        "knn_rows": n_knn - m, "knn_table_sha256_equal": sha(knn_ref) == sha(table[: n_knn - m]),
+        "knn_oracle_s": round(knn_s, 2),
+        "gate": "rel_err <= 1e-9 (BASELINE north_star)",
+    }
+    model, nproc = cpu_info()
+    base = {"value": 1.0 / sec_per_eval, "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": sample, "cpu_model": model, "nproc": nproc, "note": PORT_NOTE}
+    return base, parity
 
 
 # ------------------------------------------------------------------ arms
+
+def config_key(args):
+    return f"n{args.n}_m{args.m}_nu{args.nu}_{args.locations}_{args.ordering}"
+
+
+def ncu_traffic(args):
+    """DRAM bytes per launch of THIS config's dominant kernel, from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), or None if never captured."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            rec = json.load(f).get(config_key(args))
+    except (OSError, ValueError):
+        return None, None
+    if not rec:
+        return None, None
+    return rec.get("dram_bytes_per_launch"), rec.get("source")
+
 
 def run_reference(args, rank, world):
     """`--impl reference`: the reference algorithm on host cores (oracle port)."""
@@ -193,15 +293,16 @@ def run_reference(args, rank, world):
     from oracle import oracle as O
 
     # (the reference has no maxmin ordering; its per-block cost does not
-    # depend on the ordering, so the sample is randomly ordered)
-    locs, y = synthetic(args.n, kind=args.locations)
+    # depend on the ordering or on the observation values, so the sample is
+    # randomly ordered with N(0,1) observations — no GPU on this arm)
+    locs = synthetic(args.n, kind=args.locations)
+    y = np.random.default_rng(Y_SEED).standard_normal(args.n)
     perm = np.random.default_rng(0).permutation(args.n)
     ol, oy = locs[perm], y[perm]
-    # the reference's own (CPU) conditioning-set search on the prefix actually timed
     threads = os.cpu_count() or 1
     m = args.m
     t0 = time.perf_counter()
-    n_cal = min(args.n, 20000)
+    n_cal = min(args.n, 20000 if args.nu in (0.5, 1.5, 2.5) else 3000)
     table_cal = O.knn_pred(ol[:n_cal], m, threads)
     r = O.loglik(ol[:n_cal], oy[:n_cal], m, table_cal, "matern", 1.0, args.beta, args.nu, threads)
     per_block = (time.perf_counter() - t0) / (n_cal - m + 1)
@@ -218,21 +319,43 @@ def run_reference(args, rank, world):
         if i >= args.warmup:
             times.append(dt)
     blocks_s = n_s - m + 1
-    sec_per_eval = statistics.mean(times) / blocks_s * (args.n - m + 1)
+    step_s = statistics.mean(times)
+    sec_per_eval = step_s / blocks_s * (args.n - m + 1)
     value = 1.0 / sec_per_eval
-    sample = (f"prefix n'={n_s} of the ordered c2 problem ({blocks_s} blocks per step), "
-              f"extrapolated per block to n={args.n}")
+    sample = (f"prefix n'={n_s} of the ordered problem ({blocks_s} of {args.n - m + 1} blocks "
+              f"per step, {step_s:.2f} s), extrapolated per block to n={args.n}")
+    model, nproc = cpu_info()
     line = {
         "impl": "reference", "metric": "vecchia_loglik_evals_per_s", "value": value,
         "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * sec_per_eval, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1000.0 * step_s, "ms_per_eval_extrapolated": 1000.0 * sec_per_eval,
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": model, "nproc": nproc,
+                         "note": PORT_NOTE},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+VARIANT_NAMES = {0: "generic", 1: "warp-dmma-allreg", 2: "warp-dmma-grouped",
+                 3: "warp-specialised", 4: "warp-specialised+dcache", 7: "ws-scheduler-aware",
+                 8: "ws-scheduler-aware+dcache", 11: "large-m-cta", 12: "large-m-cta+dcache",
+                 13: "thread-per-block"}
+
+
+def roofline(args, k_avg_ms, flops, n_gpus=1):
+    peak, peak_src = fp64_peak()
+    achieved = flops / (k_avg_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic(args)
+    return {"bound": "tensor", "pipe": "fp64 (DMMA + DFMA share one pipe)", "achieved": achieved,
+            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": traffic_src, "peak_source": peak_src,
+            "algorithmic": "flop_count(n,m)=(n-m+1)(m^3/3+2m^2+4m) per launch "
+                           "(vg/vecchia.py:241-251), covariance generation excluded",
+            "kernel_ms": k_avg_ms}
 
 
 def run_ours_single(args):
@@ -243,11 +366,13 @@ def run_ours_single(args):
     dev = 0
     vg._native.set_device(dev)
     torch.cuda.set_device(dev)
-    locs, y = synthetic(args.n, kind=args.locations)
-    data = vg.Dataset(locs, y)
+    locs = synthetic(args.n, kind=args.locations)
     t0 = time.perf_counter()
-    plan = vg.make_plan(data, args.m, args.ordering, seed=0)
+    plan = vg.make_plan(vg.Dataset(locs, np.zeros(args.n)), args.m, args.ordering, seed=0)
     knn_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    data = simulated_dataset(vg, locs, plan, args)
+    sim_s = time.perf_counter() - t0
     spec = vg.KernelSpec("matern", vg.KernelParams(1.0, args.beta, args.nu))
     dp = plan.device_plan(dev)
     dp.set_data(data)
@@ -295,34 +420,27 @@ def run_ours_single(args):
     h2d = args.n * 16 + args.n * 8
     d2h = 3 * (args.n - args.m) * 8 + 24
 
-    flops = flop_count(args.n, args.m)
-    achieved = flops / (k_avg_ms * 1e-3) / 1e12
+    rl = roofline(args, k_avg_ms, flop_count(args.n, args.m))
+    rl["kernel_share"] = k_avg_ms / ms
     line = {
         "metric": "vecchia_loglik_evals_per_s", "value": 1000.0 / ms, "unit": "evals/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload(args),
-        "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA + DFMA)", "achieved": achieved,
-                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(),
-                     "peak_source": FP64_PEAK_SOURCE,
-                     "algorithmic": "flop_count(n,m)=(n-m+1)(m^3/3+2m^2+4m) per launch "
-                                    "(vg/vecchia.py:241-251), covariance generation excluded",
-                     "kernel_ms": k_avg_ms, "kernel_share": k_avg_ms / ms},
+        "roofline": rl,
         "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "paper_2403_07412_b200.vecchia_loglik(dataset, plan, spec)"},
         "gpu_launches": KERNELS_PER_EVAL * args.steps,
         "clocks": clk.summary(),
-        "plan_s": round(knn_s, 3), "total": total,
-        "kernel_variant": {0: "generic", 1: "warp-dmma-allreg", 2: "warp-dmma-grouped", 3: "warp-specialised", 4: "warp-specialised+dcache", 5: "ws-short-chain", 6: "ws-short-chain+dcache", 7: "ws-scheduler-aware", 8: "ws-scheduler-aware+dcache", 9: "ws-chain-isolated", 10: "ws-chain-isolated+dcache", 11: "large-m-cta", 12: "large-m-cta+dcache", 13: "thread-per-block"}.get(dp.kernel_variant, "?"),
+        "plan_s": round(knn_s, 3), "simulate_s": round(sim_s, 3), "total": total,
+        "kernel_variant": VARIANT_NAMES.get(dp.kernel_variant, str(dp.kernel_variant)),
     }
     if not args.no_cpu_baseline:
         ordered = data.permute(plan.permutation)
-        v, sample, secs, threads = cpu_baseline(args, ordered.locations, ordered.observations,
-                                                plan.neighbors.neighbors)
-        line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": threads, "kind": "port",
-                                "sample": sample}
+        base, parity = cpu_baseline(args, ordered, plan.neighbors.neighbors, res)
+        line["cpu_baseline"] = base
+        line["parity"] = parity
     print(json.dumps(line), flush=True)
 
 
@@ -337,11 +455,11 @@ def run_ours_multi(args, rank, world):
     torch.cuda.set_device(local)
     vg._native.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    locs, y = synthetic(args.n, kind=args.locations)
-    data = vg.Dataset(locs, y)
+    locs = synthetic(args.n, kind=args.locations)
     t0 = time.perf_counter()
-    plan = vg.make_plan(data, args.m, args.ordering, seed=0)
+    plan = vg.make_plan(vg.Dataset(locs, np.zeros(args.n)), args.m, args.ordering, seed=0)
     knn_s = time.perf_counter() - t0
+    data = simulated_dataset(vg, locs, plan, args)
     spec = vg.KernelSpec("matern", vg.KernelParams(1.0, args.beta, args.nu))
     sh = ShardedVecchia(data, plan, device=local)
     for _ in range(args.warmup):
@@ -386,11 +504,8 @@ def run_ours_multi(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": dict(workload(args), parallelism=f"blocks{world}"),
-            "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA + DFMA)", "achieved": achieved,
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(),
-                         "peak_source": FP64_PEAK_SOURCE, "kernel_ms": k_avg_ms,
-                         "note": "rank-0 shard kernel, max over ranks"},
+            "roofline": dict(roofline(args, k_avg_ms, flops_rank),
+                             note="rank-0 shard kernel, max over ranks"),
             "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s",
                     "h2d_bytes_per_step": args.n * 24, "d2h_bytes_per_step": 8 * (sh.buf.numel()),
                     "api": "paper_2403_07412_b200.distributed.ShardedVecchia"},
@@ -401,16 +516,6 @@ def run_ours_multi(args, rank, world):
         print(json.dumps(line), flush=True)
     sh.close()
     dist.destroy_process_group()
-
-
-def ncu_traffic():
-    """dram bytes per launch of the fused kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_fused_kernel.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        return None
 
 
 def main():

@@ -176,6 +176,17 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
                double* total, int64_t* fail_index, double* block_first, double* block_rest,
                double* mu_new, double* sigma_new);
 
+/* Vecchia forward simulation (data generator for model-consistent parity
+ * fixtures; the reference's generator is the dense
+ * exact.simulate_grf, vg/exact.py:47-66, capped at n <= 20000):
+ * y[0:m] = L0 z[0:m], y[t] = b_t . y[J_t] + sqrt(sigma^2 - v_t . b_t) z_t with
+ * b_t = Sigma_t^-1 v_t, for the plan's ordering and neighbour table.
+ * z, y: ORDERED (n,) host arrays.  Needs a full-range plan with data set
+ * (only its locations are read).  VGP_NOT_POSITIVE_DEFINITE with
+ * *fail_index = batch entry on a non-positive pivot. */
+int vgp_simulate(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
+                 const double* z, double* y, int64_t* fail_index);
+
 /* Shard form for multi-GPU evaluation: the plan's fixed 4096-chunk partial
  * sums of block_rest (partials: plan's chunk count, see vgp_plan_info) and,
  * when the plan holds entry 0, block_first (else 0).  Summing every shard's

@@ -1106,6 +1106,42 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
   return st;
 }
 
+int vgp_simulate(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
+                 const double* z, double* y, int64_t* fail_index) {
+  if (!plan || !z || !y) return fail(VGP_E_INVALID, "null pointer");
+  Plan* p = &plan->p;
+  if (!(p->blk_lo == 0 && p->blk_hi == p->n - p->m + 1))
+    return fail(VGP_E_INVALID, "vgp_simulate needs a plan over all blocks");
+  if (!p->has_data) return fail(VGP_E_INVALID, "plan has no data (vgp_plan_set_data)");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  DeviceGuard g(p->device);
+  double *d_z = nullptr, *d_y = nullptr;
+  unsigned long long* d_f = nullptr;
+  rc = dalloc(&d_z, p->n);
+  if (!rc) rc = dalloc(&d_y, p->n);
+  if (!rc) rc = dalloc(&d_f, 1);
+  cudaError_t e = cudaSuccess;
+  if (!rc) e = cudaMemcpyAsync(d_z, z, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream);
+  if (!rc && e == cudaSuccess) e = cudaMemsetAsync(d_f, 0xff, sizeof(unsigned long long), p->stream);
+  if (!rc && e == cudaSuccess) e = launch_simulate(*p, cp, d_z, d_y, d_f, p->stream);
+  unsigned long long hf = ~0ull;
+  if (!rc && e == cudaSuccess) e = cudaMemcpy(&hf, d_f, sizeof(hf), cudaMemcpyDeviceToHost);
+  if (!rc && e == cudaSuccess) e = cudaMemcpy(y, d_y, sizeof(double) * p->n, cudaMemcpyDeviceToHost);
+  if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("simulate: ") + cudaGetErrorString(e));
+  cudaFree(d_z);
+  cudaFree(d_y);
+  cudaFree(d_f);
+  if (rc) return rc;
+  if (hf != ~0ull) {
+    if (fail_index) *fail_index = (int64_t)hf;
+    return fail(VGP_NOT_POSITIVE_DEFINITE, "simulate: non-positive pivot");
+  }
+  if (fail_index) *fail_index = -1;
+  return VGP_OK;
+}
+
 int vgp_loglik_partials(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
                         double* partials, double* block_first, int64_t* fail_index) {
   if (!plan) return fail(VGP_E_INVALID, "null plan");

@@ -143,6 +143,12 @@ cudaError_t launch_assemble(const double2* d_pts, const double* d_obs, int m, co
 cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t n,
                            double4* d_pts, cudaStream_t stream);
 
+// Vecchia forward simulation of ordered observations (vgp_simulate.cu):
+// d_z, d_y ORDERED (n,); needs a full-range plan.  *d_fail gets the first
+// non-positive-definite entry (initialise to ~0).
+cudaError_t launch_simulate(const Plan& p, const CovParams& cp, const double* d_z, double* d_y,
+                            unsigned long long* d_fail, cudaStream_t stream);
+
 // Generic per-block likelihood kernel (any m; smem- or global-resident block).
 cudaError_t launch_loglik_generic(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                                   cudaStream_t stream);

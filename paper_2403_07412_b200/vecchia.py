@@ -40,7 +40,10 @@ class VecchiaPlan:
     neighbors: geo.NeighborTable
     metric: geo.Metric
     ordering: str = "custom"
-    _device_plans: dict = field(default_factory=dict, repr=False, compare=False)
+    # device contexts built from this plan, keyed by (device, metric); not
+    # part of the plan's value: dropped by copy/pickle and re-validated
+    # against the plan's arrays before every reuse
+    _device_plans: dict = field(default_factory=dict, init=False, repr=False, compare=False)
 
     def __post_init__(self):
         n = self.permutation.n
@@ -50,13 +53,29 @@ class VecchiaPlan:
                 f"with n={n}, m={self.m}"
             )
 
-    def device_plan(self, device: int | None = None) -> "DevicePlan":
-        """Full-range device context on `device` (created once, then reused)."""
+    def __getstate__(self):
+        state = dict(self.__dict__)
+        state["_device_plans"] = {}
+        return state
+
+    def __setstate__(self, state):
+        self.__dict__.update(state)
+        self._device_plans = {}
+
+    def device_plan(self, device: int | None = None, metric: geo.Metric | None = None) -> "DevicePlan":
+        """Full-range device context on `device` (created once, then reused
+        while m, the permutation and the neighbour table are the very objects
+        it was built from).  `metric` (default: the plan's) sets the distance
+        used by the likelihood kernels; the reference takes it from the
+        dataset (vg/vecchia.py:143)."""
         dev = N.current_device() if device is None else int(device)
-        dp = self._device_plans.get(dev)
-        if dp is None or dp.closed:
-            dp = DevicePlan(self, device=dev)
-            self._device_plans[dev] = dp
+        metric = self.metric if metric is None else metric
+        key = (dev,) + _metric_code(metric)
+        dp = self._device_plans.get(key)
+        if dp is None or dp.closed or not dp.built_from(self):
+            # a stale context is released when its last reference goes
+            dp = DevicePlan(self, device=dev, metric=metric)
+            self._device_plans[key] = dp
         return dp
 
 
@@ -111,7 +130,7 @@ class DevicePlan:
     [block_lo, block_hi) resident on one GPU (entry 0 = joint block)."""
 
     def __init__(self, plan: VecchiaPlan, device: int | None = None, block_lo: int = 0,
-                 block_hi: int | None = None):
+                 block_hi: int | None = None, metric: geo.Metric | None = None):
         n = plan.permutation.n
         m = plan.m
         if not (1 <= m < n):
@@ -122,7 +141,10 @@ class DevicePlan:
         self.n, self.m = n, m
         self.block_lo, self.block_hi = int(block_lo), block_hi
         self.full = self.block_lo == 0 and self.block_hi == count
-        metric, radius = _metric_code(plan.metric)
+        metric, radius = _metric_code(plan.metric if metric is None else metric)
+        # the objects this context was built from (identity, not value: a
+        # plan whose arrays are replaced gets a fresh context)
+        self._source = (plan.m, plan.permutation.order, plan.neighbors.neighbors)
         order = np.ascontiguousarray(plan.permutation.order, dtype=np.int64)
         table = np.ascontiguousarray(plan.neighbors.neighbors, dtype=np.int64)
         h = ctypes.c_void_p()
@@ -137,6 +159,11 @@ class DevicePlan:
     @property
     def closed(self) -> bool:
         return not self._finalizer.alive
+
+    def built_from(self, plan: VecchiaPlan) -> bool:
+        m, order, table = self._source
+        return (m == plan.m and order is plan.permutation.order
+                and table is plan.neighbors.neighbors)
 
     def close(self) -> None:
         self._finalizer()
@@ -365,9 +392,40 @@ def vecchia_loglik(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.Kernel
         return _singleton(dataset, spec)
     if plan.permutation.n != dataset.n:
         raise ValueError(f"plan built for n={plan.permutation.n}, dataset has n={dataset.n}")
-    dp = plan.device_plan()
+    dp = plan.device_plan(metric=dataset.metric)
     dp.set_data(dataset)
     return dp.loglik(spec)
+
+
+def simulate_vecchia(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.KernelSpec,
+                     seed) -> np.ndarray:
+    """Draw observations (ORIGINAL order) from the Gaussian whose exact
+    log-density is the Vecchia likelihood of `plan`:
+    y[:m] = L0 z[:m], y_t = b_t . y[J_t] + sqrt(sigma^2 - v_t . b_t) z_t in the
+    plan's order, z = numpy default_rng(seed).standard_normal(n) (ordered).
+
+    The device-scale counterpart of the reference's dense generator
+    ``exact.simulate_grf`` (vg/exact.py:47-66, capped at n <= 20000): only
+    ``dataset.locations`` are read.  Model-consistent fields keep the
+    CPU/GPU likelihood comparison well conditioned; white noise does not
+    (SURVEY.md H5)."""
+    n = dataset.n
+    if plan.permutation.n != n:
+        raise ValueError(f"plan built for n={plan.permutation.n}, dataset has n={n}")
+    z = np.random.default_rng(seed).standard_normal(n)
+    if n == 1:
+        return np.sqrt(spec.params.sigma_sq) * z
+    dp = plan.device_plan(metric=dataset.metric)
+    dp.set_data(dataset)
+    p = spec.params
+    y_ord = np.empty(n)
+    fail = np.full(1, -1, dtype=np.int64)
+    rc = N.lib.vgp_simulate(dp.handle, N.FAMILY_CODES[spec.family], float(p.sigma_sq),
+                            float(p.beta), float(p.nu), N.dptr(z), N.dptr(y_ord), N.iptr(fail))
+    N.raise_for_status(rc, int(fail[0]))
+    y = np.empty(n)
+    y[plan.permutation.order] = y_ord
+    return y
 
 
 # The package's own implementation, so callers can tell whether the module

@@ -173,6 +173,39 @@ def c1_case(with_mle: bool):
     save("c1_n20000_m30_nu05", **out)
 
 
+def mle_free_nu_case(name, n, m, nu_true, beta_true, init, seed, clustered=False):
+    """Free-nu MLE of (sigma^2, beta, nu) (vg/fit.py:140-178, free nu at :153-157):
+    BASELINE config 5's estimator at desk scale, y from the dense simulate_grf."""
+    rng = np.random.default_rng(seed)
+    if clustered:
+        centers = rng.random((20, 2))
+        k = int(0.8 * n)
+        locs = np.concatenate([centers[rng.integers(0, 20, k)] + 0.02 * rng.standard_normal((k, 2)),
+                               rng.random((n - k, 2))])
+    else:
+        locs = rng.random((n, 2))
+    spec = kernels.KernelSpec("matern", kernels.KernelParams(1.0, beta_true, nu_true))
+    y = exact.simulate_grf(locs, spec, seed + 1)
+    data = geo.Dataset(locs, y)
+    parallel.set_num_threads(os.cpu_count() or 1)
+    cfg = fit.FitConfig(objective="vecchia", m=m, ordering="random", seed=0,
+                        init=kernels.KernelParams(*init), free_nu=True)
+    t0 = time.perf_counter()
+    fr = fit.mle_estimate(data, cfg)
+    dt = time.perf_counter() - t0
+    print(f"{name}: MLE {dt:.1f}s evals={fr.evaluations} theta={fr.theta_hat}")
+    save(name, locs=locs, obs=y, m=m, init=np.array(init),
+         mle_theta=np.array([fr.theta_hat.sigma_sq, fr.theta_hat.beta, fr.theta_hat.nu]),
+         mle_loglik=fr.loglik, mle_evals=fr.evaluations, mle_converged=fr.converged,
+         mle_seconds=dt)
+
+
+def mle_cases():
+    mle_free_nu_case("mle_freenu_n2000_m20_clustered", 2000, 20, 0.8, 0.05, (0.5, 0.1, 1.0), 601,
+                     clustered=True)
+    mle_free_nu_case("mle_freenu_n5000_m30", 5000, 30, 1.2, 0.05, (1.0, 0.1, 0.5), 611)
+
+
 def sphere_cases():
     """Great-circle metric (vg/geo.py:70-79, :266-292): kNN of the reference
     (pkg/tests/test_geo.py:196-204 shape and larger), log-likelihoods with
@@ -301,6 +334,8 @@ def main():
         sphere_cases()
     if args.only in ("", "kl"):
         kl_cases()
+    if args.only == "mle":
+        mle_cases()
     if args.only in ("", "c1"):
         c1_case(args.with_mle)
 

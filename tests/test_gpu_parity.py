@@ -293,6 +293,24 @@ def test_c1_mle_matches_reference(vg):
     assert rel(fr.loglik, float(z["mle_loglik"])) <= 1e-9
 
 
+@pytest.mark.parametrize("name", golden_names("mle_freenu"))
+def test_free_nu_mle_matches_reference(vg, name):
+    """BASELINE config 5's estimator: (sigma^2, beta, nu) with free_nu
+    (vg/fit.py:153-157), general-nu Matérn on the device Bessel K path,
+    against the reference's own mle_estimate on the same data."""
+    z = load(name)
+    data = vg.Dataset(z["locs"], z["obs"])
+    cfg = vg.FitConfig(objective="vecchia", m=int(z["m"]), ordering="random", seed=0,
+                       init=vg.KernelParams(*[float(v) for v in z["init"]]), free_nu=True)
+    fr = vg.mle_estimate(data, cfg)
+    th = z["mle_theta"]
+    got = (fr.theta_hat.sigma_sq, fr.theta_hat.beta, fr.theta_hat.nu)
+    for g, r in zip(got, th):
+        assert rel(g, float(r)) <= 1e-4
+    assert rel(fr.loglik, float(z["mle_loglik"])) <= 1e-9
+    assert fr.converged == bool(z["mle_converged"])
+
+
 @pytest.mark.parametrize("name", ["ll_n3000_m60_nu15", "ll_n2000_m30_nu15", "ll_n2000_m40_nu05_s2",
                                   "ll_n1000_m20_nu25", "ll_n300_m10_nu05"])
 def test_distance_cache_is_bit_identical(vg, name):

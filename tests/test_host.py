@@ -285,3 +285,23 @@ def test_result_pool_reuses_only_dead_buffers():
     assert c.ctypes.data == addr  # now recycled
     assert c.shape == (1000,) and c.dtype == np.float64
     assert pool.take(0).shape == (0,)
+
+
+def test_plan_copy_and_pickle_drop_device_contexts():
+    """the device-context cache is not part of the plan's value."""
+    import copy
+    import dataclasses
+    import pickle
+
+    import paper_2403_07412_b200 as vg
+
+    n, m = 50, 5
+    perm = vg.Permutation(np.arange(n))
+    table = vg.NeighborTable(m=m, neighbors=np.tile(np.arange(m, dtype=np.int64), (n - m, 1)))
+    plan = vg.VecchiaPlan(m, perm, table, vg.Euclidean(), "identity")
+    plan._device_plans["sentinel"] = object()
+    for other in (pickle.loads(pickle.dumps(plan)), copy.deepcopy(plan),
+                  dataclasses.replace(plan, m=m)):
+        assert other._device_plans == {}
+        assert other.m == m and np.array_equal(other.neighbors.neighbors, table.neighbors)
+    assert "sentinel" in plan._device_plans
