@@ -70,6 +70,14 @@ int vgp_device_count(int* count);
 int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t m,
                          int64_t* neighbors);
 
+/* Rows [row_lo, row_hi) of the same table (targets m + row), for a rank
+ * that owns only those conditioning blocks (multi-GPU shards, SURVEY.md
+ * §8(e); the reference's per-target chunked scan, vg/geo.py:295-328).
+ * Only locations[0 : m + row_hi) are read; neighbors: (row_hi - row_lo, m).
+ * Bit-identical to the same rows of vgp_knn_predecessors. */
+int vgp_knn_predecessors_range(int device, const double* locations, int64_t n, int32_t m,
+                               int64_t row_lo, int64_t row_hi, int64_t* neighbors);
+
 /* Great-circle kNN — replaces numba geo._topm_sphere (vg/geo.py:266-292) as
  * called by nearest_neighbors (predecessors != 0: queries are data[m..nd),
  * candidates j < target) and nearest_points (predecessors == 0: queries
@@ -135,6 +143,14 @@ int vgp_bessel_kv(int device, double nu, const double* x, int64_t count, double*
 int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
                     const int64_t* order, const int64_t* neighbors, int64_t block_lo,
                     int64_t block_hi, vgp_plan** plan);
+
+/* Same, for a multi-GPU shard that holds only its own neighbour rows:
+ * shard_neighbors = rows [max(block_lo, 1) - 1, block_hi - 1) of the table
+ * (e.g. from vgp_knn_predecessors_range), so no rank ever materialises the
+ * full (n - m) x m table. */
+int vgp_plan_create_shard(int device, int64_t n, int32_t m, int metric, double radius,
+                          const int64_t* order, const int64_t* shard_neighbors, int64_t block_lo,
+                          int64_t block_hi, vgp_plan** out);
 
 /* Upload a dataset in ORIGINAL order (geo.Dataset, vg/geo.py:114-149):
  * locations (n, 2), observations (n,).  Permutation by `order` happens on
@@ -203,6 +219,14 @@ int vgp_loglik_partials(vgp_plan* plan, int family, double sigma_sq, double beta
  * available from vgp_plan_fetch.  Synchronises the stream before returning. */
 int vgp_loglik_partials_device(vgp_plan* plan, int family, double sigma_sq, double beta,
                                double nu, double* out);
+
+/* Raw failure keys of the plan's last evaluation, for cross-shard agreement
+ * (MIN over ranks, then decode): keys[0] = NPD key ordered like the
+ * reference's first raise — (potrf chunk of 2^21 / m^2 entries, pivot column,
+ * entry) packed as chunk << 42 | column << 24 | entry-in-chunk, or the entry
+ * itself for m > 256 (vg/batchla.py:146-164, vg/parallel.py:37-43);
+ * keys[1] = first entry with sigma_new <= 0.  UINT64_MAX = none. */
+int vgp_plan_fail_keys(vgp_plan* plan, uint64_t* keys);
 
 /* Per-kernel timing of the fused block kernel (CUDA events on the plan's
  * stream around every launch while enabled).  vgp_plan_kernel_time returns

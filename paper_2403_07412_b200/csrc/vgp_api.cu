@@ -249,9 +249,11 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
         : fast_c ? 8
         : (fast_n ? 7
                   : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
+    const bool ws4_ok = p->m >= 8;
     const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
                     ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c) ||
-                    (v == 13 && tiny);
+                    (v == 13 && tiny) || (v == 14 && fast_c && ws4_ok) ||
+                    (v == 15 && fast_n && ws4_ok);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
@@ -268,6 +270,7 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
       if (v <= 6 || v >= 9 && v <= 10) return cudaErrorNotSupported;  // retired variants
       if (v <= 8) return launch_loglik_ws3(*p, cp, lo, hi, s, v == 8);
       if (v == 13) return launch_loglik_tiny(*p, cp, lo, hi, s);
+      if (v >= 14) return launch_loglik_ws4(*p, cp, lo, hi, s, v == 14);
       return launch_loglik_big(*p, cp, lo, hi, s, v == 12);
     };
     const int64_t count = e_hi - e_lo;
@@ -341,9 +344,18 @@ int vgp_device_count(int* count) {
 
 int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t m,
                          int64_t* neighbors) {
+  if (m < 1 || n <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
+  return vgp_knn_predecessors_range(device, locations, n, m, 0, n - m, neighbors);
+}
+
+int vgp_knn_predecessors_range(int device, const double* locations, int64_t n, int32_t m,
+                               int64_t row_lo, int64_t row_hi, int64_t* neighbors) {
   if (!locations || !neighbors) return fail(VGP_E_INVALID, "null pointer");
   if (m < 1 || n <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
   if (n > (int64_t)INT32_MAX) return fail(VGP_E_INVALID, "n exceeds int32 index range");
+  if (row_lo < 0 || row_hi > n - m || row_lo > row_hi) return fail(VGP_E_INVALID, "row range outside [0, n - m)");
+  if (row_lo == row_hi) return VGP_OK;
+  n = m + row_hi;  // later points are never candidates of these targets
   int rc = check_device(device);
   if (rc) return rc;
   DeviceGuard g(device);
@@ -353,7 +365,7 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
   int64_t* d_out = nullptr;
   double* d_keys = nullptr;
   int32_t* d_idx = nullptr;
-  const int64_t nq = n - m;
+  const int64_t nq = row_hi - row_lo;
   // grid-pruned search past ~200k points (env VGP_KNN_GRID_MIN overrides);
   // both paths produce the same table bit for bit
   int64_t grid_min = 200000;
@@ -362,7 +374,7 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
     rc = dalloc(&d_pts, n);
     cudaError_t e = cudaSuccess;
     if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
-    if (!rc && e == cudaSuccess) e = knn_pred_grid(d_pts, locations, n, m, 32768, neighbors, s);
+    if (!rc && e == cudaSuccess) e = knn_pred_grid(d_pts, locations, n, m, 32768, neighbors, s, row_lo, row_hi);
     if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn (grid): ") + cudaGetErrorString(e));
     cudaFree(d_pts);
@@ -379,7 +391,7 @@ int vgp_knn_predecessors(int device, const double* locations, int64_t n, int32_t
   if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
   for (int64_t q0 = 0; !rc && e == cudaSuccess && q0 < nq; q0 += batch) {
     int64_t qn = std::min(batch, nq - q0);
-    e = launch_knn(d_pts, n, d_pts + m + q0, qn, q0, 1, m, d_out, d_keys, d_idx, s);
+    e = launch_knn(d_pts, n, d_pts + m + row_lo + q0, qn, row_lo + q0, 1, m, d_out, d_keys, d_idx, s);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(neighbors + q0 * m, d_out, sizeof(int64_t) * qn * m,
                           cudaMemcpyDeviceToHost, s);
@@ -657,9 +669,27 @@ int vgp_bessel_kv(int device, double nu, const double* x, int64_t count, double*
   return rc;
 }
 
+static int plan_create(int device, int64_t n, int32_t m, int metric, double radius,
+                       const int64_t* order, const int64_t* shard_rows, int64_t block_lo,
+                       int64_t block_hi, vgp_plan** out);
+
 int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
                     const int64_t* order, const int64_t* neighbors, int64_t block_lo,
                     int64_t block_hi, vgp_plan** out) {
+  const int64_t rest_lo = std::max<int64_t>(block_lo, 1) - 1;
+  return plan_create(device, n, m, metric, radius, order,
+                     neighbors ? neighbors + rest_lo * (int64_t)m : nullptr, block_lo, block_hi, out);
+}
+
+int vgp_plan_create_shard(int device, int64_t n, int32_t m, int metric, double radius,
+                          const int64_t* order, const int64_t* shard_neighbors, int64_t block_lo,
+                          int64_t block_hi, vgp_plan** out) {
+  return plan_create(device, n, m, metric, radius, order, shard_neighbors, block_lo, block_hi, out);
+}
+
+static int plan_create(int device, int64_t n, int32_t m, int metric, double radius,
+                       const int64_t* order, const int64_t* neighbors, int64_t block_lo,
+                       int64_t block_hi, vgp_plan** out) {
   if (!out || !order) return fail(VGP_E_INVALID, "null pointer");
   *out = nullptr;
   if (m < 1 || n <= m) return fail(VGP_E_INVALID, "need 1 <= m < n");
@@ -778,7 +808,7 @@ int vgp_plan_create(int device, int64_t n, int32_t m, int metric, double radius,
   if (e == cudaSuccess && nrest > 0) {
     // int64 -> int32 neighbour rows of this shard, via the pinned stage
     std::vector<int32_t> tmp((size_t)nrest * m);
-    const int64_t* src = neighbors + rest_lo * (int64_t)m;
+    const int64_t* src = neighbors;  // rows [rest_lo, rest_hi)
     for (size_t i = 0; i < tmp.size(); ++i) {
       int64_t v = src[i];
       if (v < 0 || v >= n) {
@@ -1037,7 +1067,7 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 13) return fail(VGP_E_INVALID, "bad variant");
+  if (!plan || variant < -1 || variant > 15) return fail(VGP_E_INVALID, "bad variant");
   // -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
   // 3 warp-specialised DMMA, 4 warp-specialised streaming the distance cache
   plan->p.force_variant = variant;
@@ -1104,6 +1134,15 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
   if (total) *total = st == VGP_OK ? sc[0] : NAN;
   if (block_first) *block_first = st == VGP_OK ? sc[1] : NAN;
   return st;
+}
+
+int vgp_plan_fail_keys(vgp_plan* plan, uint64_t* keys) {
+  if (!plan || !keys) return fail(VGP_E_INVALID, "null pointer");
+  Plan* p = &plan->p;
+  DeviceGuard g(p->device);
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  VGP_CUDA_TRY(cudaMemcpy(keys, p->d_fail, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return VGP_OK;
 }
 
 int vgp_simulate(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,

@@ -116,7 +116,7 @@ cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* 
 // Predecessor kNN by index batches with a grid over the earlier points
 // (vgp_knn.cu), bit-identical to launch_knn; h_locs / h_out on the host.
 cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n, int32_t m, int64_t batch,
-                          int64_t* h_out, cudaStream_t st);
+                          int64_t* h_out, cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = -1);
 
 // The same for great-circle plans: points (lambda, phi, cos phi, 0) on the device.
 cudaError_t knn_pred_grid_sphere(const double4* d_pts, int64_t n, int32_t m, int64_t batch, int64_t* h_out,
@@ -176,6 +176,10 @@ cudaError_t launch_loglik_big(const Plan& p, const CovParams& cp, int64_t e_lo, 
                               cudaStream_t stream, bool cache);
 // Scheduler-aware layout: one worker warp per SM sub-partition serving the
 // two blocks whose chain warps share that sub-partition (vgp_ws3_kernel.cuh).
+// Split-scheduler variant: chain + generation warps on schedulers 0, 1,
+// DMMA update warps on 2, 3 (vgp_ws4_kernel.cuh); 8 <= m, m + 2 <= 64.
+cudaError_t launch_loglik_ws4(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                              cudaStream_t stream, bool cache);
 cudaError_t launch_loglik_ws3(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream, bool cache);
 

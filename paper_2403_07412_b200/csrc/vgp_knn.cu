@@ -268,7 +268,11 @@ namespace vgp {
 // points; bit-identical to launch_knn's brute force (see grid_query_kernel).
 // locations are the ORDERED points (host); out (n - m) x m on the host.
 cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n, int32_t m, int64_t batch,
-                          int64_t* h_out, cudaStream_t st) {
+                          int64_t* h_out, cudaStream_t st, int64_t row_lo, int64_t row_hi) {
+  // rows [row_lo, row_hi) of the table (targets m + row); only points
+  // [0, m + row_hi) are ever candidates
+  if (row_hi < 0) row_hi = n - m;
+  n = m + row_hi;
   double x0 = h_locs[0], x1 = h_locs[0], y0 = h_locs[1], y1 = h_locs[1];
   for (int64_t i = 0; i < n; ++i) {
     x0 = std::min(x0, h_locs[2 * i]);
@@ -276,7 +280,7 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
     y0 = std::min(y0, h_locs[2 * i + 1]);
     y1 = std::max(y1, h_locs[2 * i + 1]);
   }
-  const int64_t nqmax = std::min<int64_t>(batch, n - m);
+  const int64_t nqmax = std::max<int64_t>(1, std::min<int64_t>(batch, row_hi - row_lo));
   const int64_t slots = ((nqmax + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
   const int gmax = 4096;
   uint32_t *cell = nullptr, *cell_s = nullptr;
@@ -300,7 +304,7 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
   A((void**)&cnt, sizeof(int) * slots);
   A((void**)&out, sizeof(int64_t) * nqmax * m);
   A(&tmp, tmp_bytes);
-  for (int64_t s0 = m; e == cudaSuccess && s0 < n; s0 += batch) {
+  for (int64_t s0 = m + row_lo; e == cudaSuccess && s0 < n; s0 += batch) {
     const int64_t e0 = std::min(n, s0 + batch), nq = e0 - s0;
     // grid over [0, s0): about 3 points per cell
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t)std::sqrt((double)s0 / 3.0)));
@@ -339,7 +343,7 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
       e = cudaGetLastError();
     }
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(h_out + (s0 - m) * m, out, sizeof(int64_t) * nq * m, cudaMemcpyDeviceToHost, st);
+      e = cudaMemcpyAsync(h_out + (s0 - m - row_lo) * m, out, sizeof(int64_t) * nq * m, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
   cudaFreeAsync(cell, st);

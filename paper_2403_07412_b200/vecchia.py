@@ -79,8 +79,8 @@ class VecchiaPlan:
         return dp
 
 
-def make_plan(dataset: geo.Dataset, m: int, ordering: str = "random", seed: int = 0) -> VecchiaPlan:
-    """Build the ordering and preceding-neighbor table for a dataset (vg/vecchia.py:59-82)."""
+def make_ordering(dataset: geo.Dataset, ordering: str = "random", seed: int = 0) -> geo.Permutation:
+    """The ordering step of make_plan (vg/vecchia.py:62-75)."""
     n = dataset.n
     if ordering not in ORDERINGS:
         raise ValueError(f"unknown ordering {ordering!r}; expected one of {ORDERINGS}")
@@ -94,6 +94,13 @@ def make_plan(dataset: geo.Dataset, m: int, ordering: str = "random", seed: int 
         perm = geo.maxmin_ordering(dataset.locations)
     else:
         perm = geo.Permutation(np.arange(n))
+    return perm
+
+
+def make_plan(dataset: geo.Dataset, m: int, ordering: str = "random", seed: int = 0) -> VecchiaPlan:
+    """Build the ordering and preceding-neighbor table for a dataset (vg/vecchia.py:59-82)."""
+    n = dataset.n
+    perm = make_ordering(dataset, ordering, seed)
     if n == 1:
         table = geo.NeighborTable(m=0, neighbors=np.empty((0, 0), dtype=np.int64))
         return VecchiaPlan(0, perm, table, dataset.metric, ordering)
@@ -148,8 +155,18 @@ class DevicePlan:
         order = np.ascontiguousarray(plan.permutation.order, dtype=np.int64)
         table = np.ascontiguousarray(plan.neighbors.neighbors, dtype=np.int64)
         h = ctypes.c_void_p()
-        N.check(N.lib.vgp_plan_create(self.device, n, m, metric, radius, N.iptr(order),
-                                      N.iptr(table), self.block_lo, self.block_hi, ctypes.byref(h)))
+        rows = getattr(plan, "row_lo", None)
+        if rows is not None:
+            # a ShardPlan holds only the neighbour rows of its own blocks
+            if (max(self.block_lo, 1) - 1, self.block_hi - 1) != (plan.row_lo, plan.row_hi):
+                raise ValueError("shard plan rows do not match the block range")
+            N.check(N.lib.vgp_plan_create_shard(self.device, n, m, metric, radius, N.iptr(order),
+                                                N.iptr(table), self.block_lo, self.block_hi,
+                                                ctypes.byref(h)))
+        else:
+            N.check(N.lib.vgp_plan_create(self.device, n, m, metric, radius, N.iptr(order),
+                                          N.iptr(table), self.block_lo, self.block_hi,
+                                          ctypes.byref(h)))
         self._h = h
         self._finalizer = weakref.finalize(self, _release, h.value)
         info = self.info()

@@ -97,3 +97,126 @@ def test_ordered_total_matches_reference_rule():
     for p in vec[1:]:
         s += p
     assert ordered_total(vec) == vec[0] + s
+
+
+# ---------------------------------------------------------------- sharded MLE
+
+class _OracleShard:
+    """A ShardObjective whose per-rank fill is the CPU oracle over this rank's
+    blocks (test infrastructure standing in for the GPU shard): the package's
+    own collective, ordered total and failure agreement run unchanged."""
+
+    def __new__(cls, locs, y, m, table, dist_mod, torch_mod):
+        from paper_2403_07412_b200.distributed import ShardObjective
+
+        class Impl(ShardObjective):
+            def __init__(self):
+                super().__init__(locs.shape[0], m, None, dist_mod, torch_mod, "cpu")
+                self.last = None
+
+            def _fill(self, spec):
+                from oracle import oracle as O
+
+                p = spec.params
+                r = O.loglik(locs, y, m, table, spec.family, p.sigma_sq, p.beta, p.nu, threads=1)
+                self.last = r
+                self.send.zero_()
+                lo, hi = self.block_lo, self.block_hi
+                if r.status != 0:
+                    if hi > lo:
+                        self.send[1 + (max(lo, 1) - 1) // CHUNK] = float("nan")
+                    return
+                if lo == 0:
+                    self.send[0] = r.block_first
+                k_lo, k_hi = max(lo, 1) - 1, hi - 1
+                for c in range(k_lo // CHUNK, (k_hi + CHUNK - 1) // CHUNK):
+                    a, b = c * CHUNK, min((c + 1) * CHUNK, self.n - m)
+                    self.send[1 + c] = O.pairwise_sum(r.block_rest[a:b])
+
+            def _failure_keys(self):
+                from paper_2403_07412_b200.distributed import NO_FAILURE
+
+                r = self.last
+                lo, hi = self.block_lo, self.block_hi
+                if r is None or r.status == 0 or not (lo <= r.fail_index < hi):
+                    return NO_FAILURE, NO_FAILURE
+                if r.status == 2:
+                    return NO_FAILURE, r.fail_index
+                chunk = max(1, (1 << 21) // (m * m))  # pivot column unknown here: 0
+                e = r.fail_index
+                return ((e // chunk) << 42) | (e % chunk), NO_FAILURE
+
+        return Impl()
+
+
+def _mle_worker(rank, world, port, n, m, out_path):
+    import paper_2403_07412_b200 as vg
+    from paper_2403_07412_b200.distributed import mle_estimate_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    locs, y, table = _problem(n, m)
+    data = vg.Dataset(locs, y)
+    cfg = vg.FitConfig(objective="vecchia", m=m, ordering="identity", seed=0,
+                       init=vg.KernelParams(0.5, 0.05, 0.5), max_evals=120)
+    ev = _OracleShard(locs, y, m, table, dist, torch)
+    fr = mle_estimate_sharded(data, cfg, evaluator=ev)
+    np.save(out_path + f".{rank}.npy", np.array([fr.theta_hat.sigma_sq, fr.theta_hat.beta,
+                                                  fr.loglik, fr.evaluations]))
+    dist.destroy_process_group()
+
+
+def test_sharded_mle_matches_single_process(tmp_path):
+    """mle_estimate_sharded at world size 2: every rank follows the single-
+    process Nelder-Mead trajectory (vg/fit.py:61-137) bit for bit, because
+    every sharded total equals the single-process total bit for bit."""
+    import paper_2403_07412_b200 as vg
+    from oracle import oracle as O
+
+    n, m, world = 9000, 10, 2
+    out = str(tmp_path / "mle")
+    mp.spawn(_mle_worker, args=(world, _free_port(), n, m, out), nprocs=world, join=True)
+    locs, y, table = _problem(n, m)
+    data = vg.Dataset(locs, y)
+    cfg = vg.FitConfig(objective="vecchia", m=m, ordering="identity", seed=0,
+                       init=vg.KernelParams(0.5, 0.05, 0.5), max_evals=120)
+
+    def single(spec):
+        p = spec.params
+        r = O.loglik(locs, y, m, table, spec.family, p.sigma_sq, p.beta, p.nu, threads=1)
+        if r.status != 0:
+            raise vg.LikelihoodEvaluationError(r.fail_index)
+        return r.total
+
+    fr = vg.mle_estimate(data, cfg, objective_fn=single)
+    ref = np.array([fr.theta_hat.sigma_sq, fr.theta_hat.beta, fr.loglik, fr.evaluations])
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(out + f".{r}.npy"), ref)
+
+
+def _fail_worker(rank, world, port, out_path):
+    import paper_2403_07412_b200 as vg
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # duplicated point at ordered index 9000 > the first shard: the failure
+    # sits on rank 1 and every rank must raise the same index
+    n, m = 13000, 12
+    locs, y, table = _problem(n, m)
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, 0.08, 0.5))
+    locs[9000] = locs[int(table[9000 - m][0])]  # the target duplicates its nearest neighbour
+    ev = _OracleShard(locs, y, m, table, dist, torch)
+    try:
+        ev.total(spec)
+        res = -1
+    except vg.LikelihoodEvaluationError as exc:
+        res = exc.block_index if hasattr(exc, "block_index") else exc.args[0]
+    np.save(out_path + f".{rank}.npy", np.array([res]))
+    dist.destroy_process_group()
+
+
+def test_sharded_failure_raises_on_every_rank(tmp_path):
+    out = str(tmp_path / "fail")
+    mp.spawn(_fail_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = [int(np.load(out + f".{r}.npy")[0]) for r in range(2)]
+    assert got[0] == got[1] and got[0] > 0

@@ -2,7 +2,7 @@
 reference's own tests (pkg/tests/test_exact.py) restated, plus golden values
 produced by the reference (tests/golden/make_golden.py --only kl).  The
 Vecchia side of every KL value runs the fused kernel; the dense side runs
-cuSOLVER.  Tolerances: log-likelihoods relative <= 1e-10, KL absolute
+host LAPACK.  Tolerances: log-likelihoods relative <= 1e-10, KL absolute
 <= 1e-8 (a difference of two ~1e3 numbers)."""
 
 import math
@@ -172,7 +172,7 @@ class TestKLVecchia:
 
 
 def test_mle_exact_objective_runs_on_device(vg):
-    """FitConfig(objective='exact') maximises the dense cuSOLVER likelihood
+    """FitConfig(objective='exact') maximises the dense (host LAPACK) likelihood
     and lands near the Vecchia estimate at full conditioning."""
     rng = np.random.default_rng(12)
     locs = rng.random((300, 2))
