@@ -19,6 +19,11 @@
 //            tile against L_cc (row per lane, L_cc broadcast from shared
 //            memory) and writes L back in DMMA-operand order.
 //
+// The block's points (x, y, obs, 0: 32-byte rows) are gathered by TMA
+// (cp.async.bulk.tensor.2d tile::gather4, SASS UTMALDG.2D.GATHER4: each lane
+// of warp 1 brings 4 rows by index) into shared memory while the previous
+// block finishes, so no block starts on a dependent global-load chain.
+//
 // Tiles live in the ws:: swizzled layout (conflict-free fragment and row
 // accesses): in shared memory while the tile triangle fits (m <= ~200,
 // several CTAs per SM overlap one block's serial diagonal phase with the
@@ -27,6 +32,8 @@
 // from HBM with coalesced 512-byte tile loads) or from the gathered
 // coordinates.
 #pragma once
+
+#include <cuda.h>
 
 #include "vgp_math.cuh"
 #include "vgp_ws_kernel.cuh"
@@ -50,15 +57,28 @@ constexpr int kThreads = 32 * kWarps;
 constexpr int kGroup = 4;  // tiles per warp in flight
 constexpr int kHead = 256 + 64 + 8 + 5 * kBesselTab;  // exp table | Lt | Iv | Bessel tables
 
-__host__ __device__ inline int ntiles_of(int m) { return (m + 2 + 7) / 8; }
+__host__ __device__ constexpr int ntiles_of(int m) { return (m + 2 + 7) / 8; }
 // doubles of the shared-memory area besides the tiles
 // the Bessel tables only exist for general nu: the closed forms keep 2.5 KB
-// more shared memory per CTA (m = 120: 75.4 KB, 3 CTAs per SM instead of 2)
+// more shared memory per CTA (m = 120: 74.6 KB, 3 CTAs per SM instead of 2)
 __host__ __device__ constexpr int head_fixed(int kind) {
   return 256 + 64 + 8 + (kind == kMaternGen ? 5 * kBesselTab : 0);
 }
+// head | G: the block's points, 32-byte rows (P of them), 128-byte aligned
+// for the TMA gather | mbarrier (+ pad)
+__host__ __device__ constexpr int g_offset(int kind) { return (head_fixed(kind) + 15) & ~15; }
 __host__ __device__ inline int head_doubles(int m, int kind = kMaternGen) {
-  return head_fixed(kind) + 3 * 8 * ntiles_of(m) + 4;
+  return g_offset(kind) + 4 * 8 * ntiles_of(m) + 2;
+}
+
+// one 4-row TMA gather of 32-byte point rows into shared memory (tile::gather4)
+__device__ __forceinline__ void gather4(void* dst, const CUtensorMap* map, int r0, int r1, int r2,
+                                        int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dmma::smem_u32(dst)),
+      "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(dmma::smem_u32(bar))
+      : "memory");
 }
 __host__ __device__ inline int64_t tile_doubles(int m) {
   const int nt = ntiles_of(m);
@@ -87,25 +107,27 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
   return cov_ref(cp, d);
 }
 
-template <int KIND, bool CACHE, bool GT>
+template <int KIND, bool CACHE, bool GT, int MC = 0>
 __global__ void __launch_bounds__(kThreads, GT ? 3 : 4)
-loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
-                  int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
+loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __restrict__ nbr,
+                  int m_rt, int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
                   const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch) {
-  const int NT = ntiles_of(m);
+  // MC > 0: conditioning size fixed at compile time (tile counts and
+  // addresses fold to constants)
+  const int m = MC > 0 ? MC : m_rt;
+  const int NT = MC > 0 ? ntiles_of(MC) : ntiles_of(m);
   const int P = 8 * NT;
   const double s2 = cp.s2;
   const int NC = (m + 8) >> 3;  // tile columns holding pivots or the Schur column
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   double* tabw = smem;
   double* Lt = smem + 256;  // L_cc transposed: Lt[8k + j] = L[j][k]
   double* Iv = Lt + 64;     // reciprocal pivots
   double* Bt = Iv + 8;      // general-nu Bessel reciprocal tables
-  double* O = smem + head_fixed(KIND);  // yJ row (row m+1)
-  double2* XY = reinterpret_cast<double2*>(O + P);
-  double* Y = O + 3 * P;  // target observation
+  double4* G = reinterpret_cast<double4*>(smem + g_offset(KIND));  // the block's points
+  uint64_t* gbar = reinterpret_cast<uint64_t*>(smem + g_offset(KIND) + 4 * P);
   double* T = GT ? gscratch + (size_t)blockIdx.x * tile_doubles(m) : smem + head_doubles(m, KIND);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -114,24 +136,44 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tabw[i] = s2 * kExp2Table[i];
   if (KIND == kMaternGen) bessel_fill_tab(cp, Bt, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dmma::smem_u32(gbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   const double* tab = smem;
   auto tile = [&](int I, int J) -> double* { return T + (size_t)tidx(I, J, NT) * 64; };
+  // block eb's point rows: lane l of warp 1 gathers rows 4l..4l+3 (P / 4 <= 32
+  // lanes per pass): neighbours a < m, the target at a = m, row 0 as padding
+  const uint32_t gbytes = (uint32_t)(P * sizeof(double4));
+  auto row_of = [&](int64_t eb, int a) -> int {
+    if (a < m) return nbr[(eb - 1 - rest_lo) * (int64_t)m + a];
+    return a == m ? (int)(m + eb - 1) : 0;
+  };
+  auto issue_gather = [&](int64_t eb) {
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dmma::smem_u32(gbar)),
+                   "r"(gbytes)
+                   : "memory");
+    __syncwarp();
+    for (int a0 = 4 * lane; a0 < P; a0 += 128)
+      gather4(G + a0, &pmap, row_of(eb, a0), row_of(eb, a0 + 1), row_of(eb, a0 + 2),
+              row_of(eb, a0 + 3), gbar);
+  };
+  uint32_t gpar = 0;
+  if (warp == 1 && e_lo + blockIdx.x < e_hi) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue_gather(e_lo + blockIdx.x);
+  }
 
   int fj = -1;  // warp 0: first non-positive pivot column of the current block
   for (int64_t e = e_lo + blockIdx.x; e < e_hi; e += gridDim.x) {
     const double* D = CACHE ? dcache + (e - 1 - rest_lo) * cstride : nullptr;
-    // ---- gather: yJ row, target observation (and coordinates)
-    for (int a = threadIdx.x; a < P; a += blockDim.x) {
-      double4 p = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (a < m) p = pts[nbr[(e - 1 - rest_lo) * (int64_t)m + a]];
-      else if (a == m) p = pts[m + e - 1];
-      O[a] = a < m ? p.z : 0.0;
-      if (a == m) Y[0] = p.z;
-      if (!CACHE) XY[a] = make_double2(p.x, p.y);
-    }
+    // ---- this block's points (gathered while the previous block finished)
+    dmma::mbar_wait(gbar, gpar);
+    gpar ^= 1;
+    const double y_t = G[m].z;  // target observation (G is refilled before the last panel)
     fj = -1;
-    __syncthreads();
 
     // tile column J of the block: generate the tiles (I, J), I >= J, dealt
     // round-robin over warps [w0, w0 + nw) in groups of kGroup (inactive
@@ -147,23 +189,24 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             if (I < NT) {
               const int i = 8 * I + r;
               double v0, v1;
+              const int j0 = 8 * J + 2 * q;  // columns j0, j0 + 1
               if (CACHE) {
                 const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, J, NT) * 64 + chunk_off(r, q)));
                 v0 = cov_any<KIND>(dv.x, cp, tab, Bt);
                 v1 = cov_any<KIND>(dv.y, cp, tab, Bt);
               } else {
-                const double2 pa = XY[i < P ? i : 0];
-                const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * J + 2 * q);
-                double dx = pa.x - pb.x, dy = pa.y - pb.y;
+                const double2 pa = *reinterpret_cast<const double2*>(G + (i < P ? i : 0));
+                const double2 pb0 = *reinterpret_cast<const double2*>(G + j0);
+                const double2 pb1 = *reinterpret_cast<const double2*>(G + j0 + 1);
+                double dx = pa.x - pb0.x, dy = pa.y - pb0.y;
                 v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
-                dx = pa.x - pb.z;
-                dy = pa.y - pb.w;
+                dx = pa.x - pb1.x;
+                dy = pa.y - pb1.y;
                 v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
               }
               if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
-                const double2 ov = ld2(O + 8 * J + 2 * q);
-                v0 = i == m + 1 ? ov.x : 0.0;
-                v1 = i == m + 1 ? ov.y : 0.0;
+                v0 = (i == m + 1 && j0 < m) ? G[j0].z : 0.0;
+                v1 = (i == m + 1 && j0 + 1 < m) ? G[j0 + 1].z : 0.0;
               }
               acc[g][0] = v0;
               acc[g][1] = v1;
@@ -224,6 +267,13 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
       } else if (c > 0) {
         column_work(c, c - 1, 0, kWarps);
         __syncthreads();
+      }
+      // the last tile column is generated: G is free, gather the next block
+      // (its points land while this block's last panels finish)
+      if (warp == 1 && c == NC - 1 && e + gridDim.x < e_hi) {
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_gather(e + gridDim.x);
       }
       // ================= diagonal tile (warp 0) =================
       if (warp == 0) {
@@ -305,7 +355,7 @@ loglik_big_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                 atomicMin(&fail[1], (unsigned long long)e);
                 rest[kk] = 0.0;
               } else {
-                const double resid = Y[0] - mu;
+                const double resid = y_t - mu;
                 rest[kk] = -0.5 * (resid * resid / sg + kLog2Pi + log(sg));
               }
             }
@@ -367,11 +417,17 @@ inline size_t smem_bytes(int m, bool gt, int kind = kMaternGen) {
 // tiles in shared memory up to ~200 KB per CTA, else the global scratch
 inline bool use_global_tiles(int m) { return smem_bytes(m, false) > 200 * 1024; }
 
-template <int KIND, bool CACHE, bool GT>
+// TMA descriptor of the plan's points: a 2-D tensor of n rows x 4 doubles
+// (x, y, obs, 0), one row per box, for tile::gather4
+bool point_map(const double4* pts, int64_t n, CUtensorMap* map);
+
+template <int KIND, bool CACHE, bool GT, int MC = 0>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, double* gscratch, int max_grid) {
+  CUtensorMap map;
+  if (!point_map(p.d_pts, p.n, &map)) return cudaErrorNotSupported;
   const size_t sm = smem_bytes(p.m, GT, KIND);
-  auto kern = loglik_big_kernel<KIND, CACHE, GT>;
+  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (err != cudaSuccess) return err;
   int per_sm = 0;
@@ -382,7 +438,7 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   int64_t cap = (int64_t)p.num_sms * per_sm;
   if (GT && cap > max_grid) cap = max_grid;
   const int grid = (int)(count < cap ? count : cap);
-  kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp,
+  kern<<<grid, kThreads, sm, stream>>>(map, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp,
                                        p.d_rest, p.d_mu, p.d_sig, p.d_fail,
                                        p.d_dcache, p.dcache_stride, gscratch);
   return cudaGetLastError();
@@ -394,9 +450,13 @@ cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_
   const bool gt = use_global_tiles(p.m);
   if (gt && !gscratch) return cudaErrorInvalidValue;
   if (cache) {
+    // config 5 (m = 60, general nu, streamed distances): compile-time m
+    if (p.m == 60 && KIND == kMaternGen) return launch<KIND, true, false, 60>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
     return gt ? launch<KIND, true, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
               : launch<KIND, true, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
   }
+  // config 4 (m = 120, closed forms, distances from coordinates): compile-time m
+  if (p.m == 120 && KIND <= kMatern25) return launch<KIND, false, false, 120>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
   return gt ? launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
             : launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
 }

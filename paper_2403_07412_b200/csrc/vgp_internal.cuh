@@ -180,6 +180,9 @@ cudaError_t launch_loglik_big(const Plan& p, const CovParams& cp, int64_t e_lo, 
 // DMMA update warps on 2, 3 (vgp_ws4_kernel.cuh); 8 <= m, m + 2 <= 64.
 cudaError_t launch_loglik_ws4(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream, bool cache);
+// Lock-step group kernel (vgp_grp_kernel.cuh): 8 <= m, m + 2 <= 64, distance cache.
+cudaError_t launch_loglik_grp(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                              cudaStream_t stream);
 cudaError_t launch_loglik_ws3(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream, bool cache);
 

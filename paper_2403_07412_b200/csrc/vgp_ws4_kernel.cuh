@@ -262,89 +262,101 @@ loglik_ws4_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
           mbar_wait(mb_col, cpar);  // column c generated and updated by the worker
           cpar ^= 1;
           mark(2 + 2 * c);
-          // lane owns panel rows R0 + lane + 32 rr: tile c + (lane + 32 rr) / 8, row lane & 7
-          constexpr int kMaxRows = 2;
-          double a[kMaxRows][8];
-          auto row_ptr = [&](int rr) -> double* {
-            const int I = c + ((lane + 32 * rr) >> 3);
-            return lastc ? S + (I - c) * 64 : T + tidx(I < NT ? I : NT - 1, c, NT) * 64;
-          };
+          // ---- diagonal tile: every lane loads it (broadcast reads) and
+          // factors it in registers, redundantly — the pivot chain then needs
+          // no cross-lane traffic at all (the row-owner chain spent half its
+          // time in the 16 shuffles per pivot); d[j][j] keeps 1 / L_jj
+          const double* dt = lastc ? S : T + tidx(c, c, NT) * 64;
+          double d[8][8];
 #pragma unroll
-          for (int rr = 0; rr < kMaxRows; ++rr) {
-            if (rr * 32 < NR) {
-              const bool ok = lane + 32 * rr < NR;
-              const double* rb = row_ptr(rr);
+          for (int i = 0; i < 8; ++i) {
 #pragma unroll
-              for (int x = 0; x < 4; ++x) {
-                double2 v = make_double2(0.0, 0.0);
-                if (ok) v = ld2(rb + chunk_off(lane & 7, x));
-                a[rr][2 * x] = v.x;
-                a[rr][2 * x + 1] = v.y;
+            for (int x = 0; x < 4; ++x) {
+              if (2 * x <= i) {
+                const double2 v = ld2(dt + chunk_off(i, x));
+                d[i][2 * x] = v.x;
+                if (2 * x + 1 <= i) d[i][2 * x + 1] = v.y;
               }
             }
           }
           if (c == 2) mark(18);
-          double lastpiv = 1.0;
-          if (jmax > 0) {
-            double piv = shfl(a[0][0], 0);
+          int fl = -1;  // first non-positive pivot of this panel
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (j < jmax) {
-                if (j == jmax - 1) lastpiv = piv;
-                const double inv = rsqrt_chain(piv);
+          for (int j = 0; j < 8; ++j) {
+            if (j < jmax) {
+              // pivot test !(piv > 0) (vg/batchla.py:146-151)
+              const double piv = d[j][j];
+              if (!(piv > 0.0) && fl < 0) fl = j;
+              const double inv = rsqrt_chain(piv);
+              d[j][j] = inv;
 #pragma unroll
-                for (int rr = 0; rr < kMaxRows; ++rr)
-                  if (rr * 32 < NR) a[rr][j] *= inv;
-                if (j + 1 < 8) {
-                  const double nxt = fma(-a[0][j], a[0][j], a[0][j + 1]);
-                  piv = shfl(nxt, j + 1);
-                }
+              for (int i = j + 1; i < 8; ++i) d[i][j] *= inv;
 #pragma unroll
-                for (int jp = j + 1; jp < 8; ++jp) {
-                  const double lc = shfl(a[0][j], jp);  // L[R0 + jp][R0 + j]
+              for (int i = j + 1; i < 8; ++i) {
 #pragma unroll
-                  for (int rr = 0; rr < kMaxRows; ++rr)
-                    if (rr * 32 < NR) a[rr][jp] = fma(-a[rr][j], lc, a[rr][jp]);
-                }
+                for (int k = j + 1; k <= i; ++k) d[i][k] = fma(-d[i][j], d[k][j], d[i][k]);
               }
             }
           }
+          if (fl >= 0 && fj < 0) fj = R0 + fl;
           if (c == 2) mark(19);
-          // pivot test !(piv > 0) (vg/batchla.py:146-151): a non-positive or
-          // NaN pivot turns every later pivot NaN, so testing the panel's
-          // last pivot detects it; the rare failing panel then locates the
-          // first bad column from the diagonal of L
-          if (!(lastpiv > 0.0) && fj < 0) {
-            double ljj = a[0][0];
+          // ---- rows below the diagonal tile: lane owns rows R0 + 8 + lane + 32 rr,
+          // forward substitution against L_cc in the order of the reference's
+          // right-looking sweep (scale by 1/L_jj, then subtract from later columns)
+          const int NB = NR - 8;
+          double mu_row = 0.0;  // last panel: column cs of row R0 + 8 (lane 0)
 #pragma unroll
-            for (int x = 1; x < 8; ++x)
-              if (lane == x) ljj = a[0][x];
-            const unsigned bad = __ballot_sync(0xffffffffu, lane < jmax && !(ljj > 0.0));
-            fj = R0 + (bad ? __ffs(bad) - 1 : jmax - 1);
+          for (int rr = 0; rr < 2; ++rr) {
+            if (rr * 32 < NB) {
+              const int lr = 8 + lane + 32 * rr;  // row within the panel
+              const bool ok = lr < NR;
+              const int I = c + (lr >> 3);
+              double* rb = lastc ? S + (I - c) * 64 : T + tidx(I < NT ? I : NT - 1, c, NT) * 64;
+              double a[8];
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                double2 v = make_double2(0.0, 0.0);
+                if (ok) v = ld2(rb + chunk_off(lane & 7, x));
+                a[2 * x] = v.x;
+                a[2 * x + 1] = v.y;
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (j < jmax) {
+                  a[j] *= d[j][j];
+#pragma unroll
+                  for (int jp = j + 1; jp < 8; ++jp) a[jp] = fma(-a[j], d[jp][j], a[jp]);
+                }
+              }
+              if (!lastc) {
+                // L rows, columns (x, x + 4) per chunk
+                if (ok) {
+#pragma unroll
+                  for (int x = 0; x < 4; ++x) st2(rb + chunk_off(lane & 7, x), a[x], a[x + 4]);
+                }
+              } else if (rr == 0) {
+                const int cs = m - R0;
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                  if (x == cs) mu_row = a[x];
+              }
+            }
           }
           if (!lastc) {
-            // L rows below the diagonal tile, columns (x, x + 4) per chunk
-#pragma unroll
-            for (int rr = 0; rr < kMaxRows; ++rr) {
-              if (rr * 32 < NR && lane + 32 * rr >= 8 && lane + 32 * rr < NR) {
-                double* rb = row_ptr(rr);
-#pragma unroll
-                for (int x = 0; x < 4; ++x)
-                  st2(rb + chunk_off(lane & 7, x), a[rr][x], a[rr][x + 4]);
-              }
-            }
             if (c == 2) mark(20);
             mbar_arrive(mb_lrdy);
             mark(3 + 2 * c);
           } else {
             // sigma_new = A[m][m], -mu = A[m+1][m] after m pivots (vg/vecchia.py:186-189, :206)
             const int cs = m - R0;
-            double v = a[0][0];
+            double sg = 0.0, nmu = 0.0;
 #pragma unroll
-            for (int x = 1; x < 8; ++x)
-              if (x == cs) v = a[0][x];
-            const double sg = shfl(v, cs);
-            const double mu = -shfl(v, cs + 1);
+            for (int x = 0; x < 8; ++x) {
+              if (x == cs) sg = d[x][x];
+              if (x + 1 < 8 && x == cs) nmu = d[x + 1][x];
+            }
+            if (cs == 7) nmu = shfl(mu_row, 0);
+            const double mu = -nmu;
             if (lane == 0) {
               const int64_t kk = e - 1 - rest_lo;
               if (fj >= 0) {

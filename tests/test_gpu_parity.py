@@ -102,16 +102,16 @@ def _plan_from_golden(vg, z):
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
-@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 7, 8, 11, 12, 13, 14, 15])
+@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 7, 8, 11, 12, 13, 14, 15, 16])
 def test_loglik_vs_reference_golden(vg, name, variant):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
     closed = str(z["family"]) == "matern" and float(z["theta"][2]) in (0.5, 1.5, 2.5)
     plane = not isinstance(_metric(vg, z), vg.GreatCircle)
     fast = closed and int(z["m"]) + 2 <= 64
-    if variant in (1, 2, 3, 4, 7, 8, 14, 15) and not fast:
+    if variant in (1, 2, 3, 4, 7, 8, 14, 15, 16) and not fast:
         pytest.skip("warp-DMMA variants cover m + 2 <= 64 closed-form Matern only")
-    if variant in (14, 15) and int(z["m"]) < 8:
+    if variant in (14, 15, 16) and int(z["m"]) < 8:
         pytest.skip("split-scheduler kernel needs two tile columns (m >= 8)")
     if variant in (1, 2, 3, 7, 11, 15) and not plane:
         pytest.skip("distances computed in the kernel are Euclidean (great circle: cached variants)")
@@ -688,3 +688,32 @@ def test_thread_per_block_reports_a_singular_block(vg):
     e = ei.value.block_index
     members = set(plan.neighbors.neighbors[e - 1].tolist()) | {m + e - 1}
     assert {1699, 1700} <= members
+
+
+# ---------------------------------------------------------------- acceptance C1
+
+def _c1_configs():
+    # pkg/tests/test_acceptance.py:43-55: the reference's 20 full-conditioning configs
+    configs = []
+    for n in (50, 200, 512):
+        for nu in (0.5, 1.5, 2.5):
+            for ordering in ("random", "morton"):
+                configs.append((n, nu, ordering, 1000 + n))
+    configs += [(512, 0.5, "random", 77), (512, 0.5, "morton", 78)]
+    return configs[:20]
+
+
+@pytest.mark.parametrize("n,nu,ordering,seed", _c1_configs())
+def test_acceptance_c1_full_conditioning_equals_dense(vg, oracle, n, nu, ordering, seed):
+    """Reference acceptance criterion 1 (pkg/tests/test_acceptance.py:43-70) on
+    the GPU: with m = n - 1 the Vecchia likelihood IS the dense one, to 1e-8
+    relative, for the reference's 20 configurations (up to m = 511, nu = 2.5)."""
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.0, 0.1, nu))
+    rng = np.random.default_rng(seed)
+    locs = rng.random((n, 2))
+    y = vg.simulate_grf(locs, spec, seed + 1)
+    data = vg.Dataset(locs, y)
+    plan = vg.make_plan(data, n - 1, ordering, seed=seed + 2)
+    approx = vg.vecchia_loglik(data, plan, spec).total
+    reference = oracle.exact_loglik(locs, y, "matern", 1.0, 0.1, nu)
+    assert rel(approx, reference) <= 1e-8
