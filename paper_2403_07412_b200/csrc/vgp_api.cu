@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "vgp_internal.cuh"
+#include "vgp_ktab.cuh"
 
 namespace vgp {
 
@@ -148,6 +149,7 @@ void free_plan(Plan* p) {
   cudaFree(p->d_work);
   cudaFree(p->d_gscratch);
   cudaFree(p->d_dcache);
+  cudaFree(p->d_ktab);
   cudaFree(p->d_prev_locs);
   cudaFree(p->d_flag);
   if (p->h_stage) cudaFreeHost(p->h_stage);
@@ -227,6 +229,16 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     const bool cached = p->d_dcache && p->dcache_valid;
     const bool fast_c = dmma_supported(p->m, cp.kind) && cached;
     const bool fast_n = dmma_supported(p->m, cp.kind) && eu;
+    // general-nu Matern: covariances from a per-evaluation polynomial table
+    // (vgp_ktab.cuh), built here once per evaluation, in the scheduler-aware
+    // kernel for m + 2 <= 64 and in the large-m kernel
+    if (cp.kind == kMaternGen && !p->no_ktab) {
+      if (!p->d_ktab) VGP_CUDA_TRY(cudaMalloc(&p->d_ktab, sizeof(double) * kKtabDoubles));
+      VGP_CUDA_TRY(launch_ktab_build(cp, p->d_ktab, s));
+    }
+    const bool gen3 = cp.kind == kMaternGen && p->d_ktab && !p->no_ktab && ws3_supported(p->m, cp.kind);
+    const bool ws3_c = (fast_c || gen3) && cached;
+    const bool ws3_n = (fast_n || gen3) && eu;
     const bool scratch_ok = !big_needs_scratch(p->m) || p->d_gscratch;
     const bool big_c = big_supported(p->m, cp.kind) && cached && scratch_ok;
     const bool big_n = big_supported(p->m, cp.kind) && eu && scratch_ok;
@@ -246,12 +258,12 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
       v = tiny ? 13
         : small && fast_n ? 1
         : (small || mid) && fast_c ? 4
-        : fast_c ? 8
-        : (fast_n ? 7
-                  : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
+        : ws3_c ? 8
+        : (ws3_n ? 7
+                 : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
     const bool ws4_ok = p->m >= 8;
-    const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3 || v == 7) && fast_n) ||
-                    ((v == 4 || v == 8) && fast_c) || (v == 11 && big_n) || (v == 12 && big_c) ||
+    const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3) && fast_n) || (v == 7 && ws3_n) ||
+                    (v == 4 && fast_c) || (v == 8 && ws3_c) || (v == 11 && big_n) || (v == 12 && big_c) ||
                     (v == 13 && tiny) || (v == 14 && fast_c && ws4_ok) ||
                     (v == 15 && fast_n && ws4_ok) || (v == 16 && fast_c && ws4_ok);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
@@ -724,6 +736,7 @@ static int plan_create(int device, int64_t n, int32_t m, int metric, double radi
   p->chunk_hi = (p->rest_hi + kReduceChunk - 1) / kReduceChunk;
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* tv = std::getenv("VGP_TUNE")) p->tune = std::atoi(tv);
+  if (const char* nk = std::getenv("VGP_NO_KTAB")) p->no_ktab = std::atoi(nk) != 0;
   p->events = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
   p->event_pool = new std::vector<cudaEvent_t>();
   const int64_t nrest = p->rest_hi - p->rest_lo;

@@ -35,6 +35,7 @@
 
 #include <cuda.h>
 
+#include "vgp_ktab.cuh"
 #include "vgp_math.cuh"
 #include "vgp_ws_kernel.cuh"
 
@@ -100,10 +101,16 @@ __device__ __noinline__ double matern_gen(double d, const CovParams& cp, const d
 // diagonal and exact duplicates, whose distance is 2^-500 by construction)
 template <int KIND>
 __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const double* tab,
-                                          const double* btab) {
+                                          const double* btab, const double* __restrict__ ktab) {
   if (KIND <= kMatern25) return cov_lean<KIND>(d, cp.inv_beta, tab);
   if (d < 1e-100) return cp.s2;
-  if (KIND == kMaternGen) return matern_gen(d, cp, btab);
+  if (KIND == kMaternGen) {
+    // per-evaluation polynomial table (vgp_ktab.cuh) when the plan built one
+    if (ktab)
+      return cov_ktab(d * cp.inv_beta, ktab, cp,
+                      [&](double u) { return cov_lean<kMatern05>(u, 1.0, tab); });
+    return matern_gen(d, cp, btab);
+  }
   return cov_ref(cp, d);
 }
 
@@ -113,7 +120,8 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
                   int m_rt, int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
-                  const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch) {
+                  const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch,
+                  const double* __restrict__ ktab) {
   // MC > 0: conditioning size fixed at compile time (tile counts and
   // addresses fold to constants)
   const int m = MC > 0 ? MC : m_rt;
@@ -192,17 +200,17 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
               const int j0 = 8 * J + 2 * q;  // columns j0, j0 + 1
               if (CACHE) {
                 const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, J, NT) * 64 + chunk_off(r, q)));
-                v0 = cov_any<KIND>(dv.x, cp, tab, Bt);
-                v1 = cov_any<KIND>(dv.y, cp, tab, Bt);
+                v0 = cov_any<KIND>(dv.x, cp, tab, Bt, ktab);
+                v1 = cov_any<KIND>(dv.y, cp, tab, Bt, ktab);
               } else {
                 const double2 pa = *reinterpret_cast<const double2*>(G + (i < P ? i : 0));
                 const double2 pb0 = *reinterpret_cast<const double2*>(G + j0);
                 const double2 pb1 = *reinterpret_cast<const double2*>(G + j0 + 1);
                 double dx = pa.x - pb0.x, dy = pa.y - pb0.y;
-                v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
+                v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt, ktab);
                 dx = pa.x - pb1.x;
                 dy = pa.y - pb1.y;
-                v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt);
+                v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt, ktab);
               }
               if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
                 v0 = (i == m + 1 && j0 < m) ? G[j0].z : 0.0;
@@ -440,7 +448,8 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   const int grid = (int)(count < cap ? count : cap);
   kern<<<grid, kThreads, sm, stream>>>(map, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp,
                                        p.d_rest, p.d_mu, p.d_sig, p.d_fail,
-                                       p.d_dcache, p.dcache_stride, gscratch);
+                                       p.d_dcache, p.dcache_stride, gscratch,
+                                       (KIND == kMaternGen && !p.no_ktab) ? p.d_ktab : nullptr);
   return cudaGetLastError();
 }
 

@@ -91,6 +91,8 @@ struct Plan {
   int tune = 0;                 // experiment selector (env VGP_TUNE at plan creation)
   double* d_gscratch = nullptr; // large-m kernel: per-CTA tile triangles (L2-resident)
   int gscratch_slots = 0;
+  double* d_ktab = nullptr;     // general-nu Matern polynomial table (vgp_ktab.cuh), per evaluation
+  bool no_ktab = false;         // env VGP_NO_KTAB: exact Bessel K in every entry (testing aid)
   double* d_dcache = nullptr;   // per-block distance cache (ws:: tile layout)
   int64_t dcache_stride = 0;    // doubles per block (16-byte multiple)
   bool dcache_valid = false;
@@ -183,6 +185,8 @@ cudaError_t launch_loglik_ws4(const Plan& p, const CovParams& cp, int64_t e_lo, 
 // Lock-step group kernel (vgp_grp_kernel.cuh): 8 <= m, m + 2 <= 64, distance cache.
 cudaError_t launch_loglik_grp(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream);
+// closed forms or general nu (table) with m + 2 <= 64
+bool ws3_supported(int m, int kind);
 cudaError_t launch_loglik_ws3(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                               cudaStream_t stream, bool cache);
 

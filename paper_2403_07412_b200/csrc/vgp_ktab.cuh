@@ -1,0 +1,73 @@
+// General-nu Matern covariance by per-evaluation piecewise polynomials.
+//
+// C(u) = s2 2^(1-nu)/Gamma(nu) u^nu K_nu(u), u = d / beta (vg/kernels.py:75-81)
+// depends on the evaluation's (s2, nu) and on u only.  Once per likelihood
+// evaluation a small kernel tabulates it (device Bessel K, vgp_math.cuh) on
+// 64 segments per binade of u, u in [2^kKtabOMin, 2^(kKtabOMax+1)): on each
+// segment a degree-7 polynomial in t in [-1, 1) interpolating at the
+// Chebyshev nodes (measured relative interpolation error <= 2e-15 against
+// scipy.special.kv, 7e-14 next to u = 2 where AMOS itself switches methods).
+// For u >= 1 the table holds C(u) e^u / s2 and the evaluation multiplies by
+// the lean s2 e^-u, so the polynomial only carries the algebraic factor; for
+// u < 1 it holds s2 - C(u), interpolated to relative accuracy (smooth kernels'
+// near-singular blocks hinge on that small deviation).
+//
+// Evaluation is integer bit work (segment = binade and top 6 mantissa bits;
+// t = u scaled into [128, 256) by exponent replacement minus an odd integer,
+// both exact), 4 x 16-byte table loads and 7 DFMA (+ the lean exp for u >= 1):
+// the cost of a closed-form Matern entry instead of a Bessel iteration.
+// u below 1e-90 (the diagonal: distance 0 or the kernels' 2^-500 guard) gives
+// s2 (vg/kernels.py:77-78); 1e-90 <= u < 2^kKtabOMin (near-duplicate points)
+// falls back to the exact device Bessel K; u beyond the table underflows to 0
+// like scipy's kv.
+#pragma once
+
+#include "vgp_internal.cuh"
+#include "vgp_math.cuh"
+
+namespace vgp {
+
+constexpr int kKtabOMin = -40;
+constexpr int kKtabOMax = 9;
+constexpr int kKtabSeg = 64;  // segments per binade
+constexpr int kKtabDeg = 7;
+constexpr int kKtabSegments = (kKtabOMax - kKtabOMin + 1) * kKtabSeg;
+constexpr int64_t kKtabDoubles = (int64_t)kKtabSegments * (kKtabDeg + 1);
+
+// exact general-nu Matern (the reference expression, not inlined: rare path)
+static __device__ __noinline__ double matern_gen_exact(double u, const CovParams& cp) {
+  if (!(u > 0.0)) return cp.s2;
+  return cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k(cp, u);
+}
+
+// C(u) from the table; e_neg(u) must return s2 * e^-u (the caller's lean exp)
+template <typename ExpNeg>
+__device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ ktab,
+                                           const CovParams& cp, ExpNeg e_neg) {
+  const int hi = __double2hiint(u);
+  const int lo = __double2loint(u);
+  const int ex = (hi >> 20) - 1023;
+  // the diagonal and exact duplicates carry distance 2^-500 (the kernels'
+  // sqrt guard) or 0: C(0) = s2 (vg/kernels.py:77-78); genuine near-duplicate
+  // distances take the exact path
+  if (ex < kKtabOMin) return u > 1e-90 ? matern_gen_exact(u, cp) : cp.s2;
+  if (ex > kKtabOMax) return 0.0;
+  const int k = (hi >> 14) & (kKtabSeg - 1);
+  const double us = __hiloint2double((hi & 0x000FFFFF) | ((1023 + 7) << 20), lo);  // [128, 256)
+  const double t = us - (double)(129 + 2 * k);
+  const double2* c = reinterpret_cast<const double2*>(ktab + (size_t)((ex - kKtabOMin) * kKtabSeg + k) * 8);
+  const double2 c01 = __ldg(c), c23 = __ldg(c + 1), c45 = __ldg(c + 2), c67 = __ldg(c + 3);
+  double p = fma(c67.y, t, c67.x);
+  p = fma(p, t, c45.y);
+  p = fma(p, t, c45.x);
+  p = fma(p, t, c23.y);
+  p = fma(p, t, c23.x);
+  p = fma(p, t, c01.y);
+  p = fma(p, t, c01.x);
+  return ex >= 0 ? p * e_neg(u) : cp.s2 - p;
+}
+
+// (re)build the table for cp (kind kMaternGen) into d_ktab (kKtabDoubles)
+cudaError_t launch_ktab_build(const CovParams& cp, double* d_ktab, cudaStream_t stream);
+
+}  // namespace vgp

@@ -39,6 +39,8 @@ __device__ __forceinline__ double point_dist(int metric, double radius, double a
 // with scipy.special.kv, the routine vg/kernels.py:81 calls, is checked in
 // tests at 1e-12 relative).  Returns 0 when e^-x underflows (u >~ 745), as
 // scipy's kv does, so s2 * coef * u^nu * K stays finite.
+// SCALED: K_nu(x) e^x instead (no under/overflow for large x; table build).
+template <bool SCALED = false>
 __device__ inline double bessel_k(const CovParams& c, double x) {
   const double eps = 1.0e-16;
   const double mu = c.mu;
@@ -72,6 +74,11 @@ __device__ inline double bessel_k(const CovParams& c, double x) {
     }
     rkmu = sum;
     rk1 = sum1 * xi2;
+    if (SCALED) {
+      const double ex = exp(x);
+      rkmu *= ex;
+      rk1 *= ex;
+    }
   } else {
     double b = 2.0 * (1.0 + x);
     double d = 1.0 / b;
@@ -98,7 +105,7 @@ __device__ inline double bessel_k(const CovParams& c, double x) {
       if (fabs(dels / s) < eps) break;
     }
     h = a1 * h;
-    rkmu = sqrt(kPi / (2.0 * x)) * exp(-x) / s;
+    rkmu = SCALED ? sqrt(kPi / (2.0 * x)) / s : sqrt(kPi / (2.0 * x)) * exp(-x) / s;
     rk1 = rkmu * (mu + x + 0.5 - h) * xi;
   }
   for (int i = 1; i <= c.nl; ++i) {

@@ -36,6 +36,7 @@
 // the yJ row, coordinates (uncached variant) and the target observation.
 #pragma once
 
+#include "vgp_ktab.cuh"
 #include "vgp_ws_kernel.cuh"
 
 namespace vgp {
@@ -64,6 +65,16 @@ constexpr int kHead = 256;   // sigma^2-scaled exp table
 constexpr int kTraceBlocks = ws::kTraceBlocks;
 constexpr int kTraceEvents = ws::kTraceEvents;
 
+// covariance at distance d: lean closed forms, or the general-nu Matern from
+// the per-evaluation polynomial table (vgp_ktab.cuh) with the same lean exp
+template <int KIND>
+__device__ __forceinline__ double cov_gen(double d, double inv_beta, const double* tab,
+                                          const double* __restrict__ ktab, const CovParams& cp) {
+  if constexpr (KIND != kMaternGen) return cov_lean<KIND>(d, inv_beta, tab);
+  return cov_ktab(d * inv_beta, ktab, cp,
+                  [&](double u) { return cov_lean<kMatern05>(u, 1.0, tab); });
+}
+
 struct SlotLayout {
   int tiles;   // doubles of the tile triangle (= cache stride)
   int stride;  // tiles | S (2 tiles) | O (P) | XY (2P) | yt (2) | mbarrier (2)
@@ -79,6 +90,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
                   const double* __restrict__ dcache, int64_t cstride,
+                  const double* __restrict__ ktab, const CovParams cpx,
                   long long* __restrict__ trace = nullptr) {
   constexpr int P = 8 * NT;
   const int m = MC > 0 ? MC : m_rt;
@@ -202,17 +214,17 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                 double v0, v1;
                 if (CACHE) {
                   const double2 dv = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
-                  v0 = cov_lean<KIND>(dv.x, inv_beta, tab);
-                  v1 = cov_lean<KIND>(dv.y, inv_beta, tab);
+                  v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx);
+                  v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx);
                 } else {
                   const double2* XY = XYb(s);
                   const double2 pa = XY[i];
                   const double4 pb = *reinterpret_cast<const double4*>(XY + 8 * c + 2 * q);
                   double dx = pa.x - pb.x, dy = pa.y - pb.y;
-                  v0 = cov_lean<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab);
+                  v0 = cov_gen<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab, ktab, cpx);
                   dx = pa.x - pb.z;
                   dy = pa.y - pb.w;
-                  v1 = cov_lean<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab);
+                  v1 = cov_gen<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), inv_beta, tab, ktab, cpx);
                 }
                 if (I == NT - 1 && i > m) {  // row m+1: yJ (0 from column m on); padding: 0
                   const double2 ov = ld2(Ob(s) + 8 * c + 2 * q);
@@ -412,7 +424,7 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   const int grid = (int)(want < cap ? want : cap);
   kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2,
                                        cp.inv_beta, p.d_rest, p.d_mu, p.d_sig, p.d_fail,
-                                       p.d_dcache, p.dcache_stride, trace);
+                                       p.d_dcache, p.dcache_stride, p.d_ktab, cp, trace);
   return cudaGetLastError();
 }
 
