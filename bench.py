@@ -436,6 +436,16 @@ def run_ours_single(args):
         "plan_s": round(knn_s, 3), "simulate_s": round(sim_s, 3), "total": total,
         "kernel_variant": VARIANT_NAMES.get(dp.kernel_variant, str(dp.kernel_variant)),
     }
+    if args.nu not in (0.5, 1.5, 2.5):
+        # general-nu Matern: covariance generation is outside the flop model
+        # (SURVEY.md H2); report its throughput beside it — distinct entries
+        # (lower triangle of Sigma_e plus v_e) per evaluation
+        per_eval = (args.n - args.m) * (args.m * (args.m + 1) // 2 + args.m)
+        line["generation"] = {"matern_entries_per_eval": per_eval,
+                              "matern_entries_per_s": per_eval * 1000.0 / ms,
+                              "method": "per-evaluation degree-7 polynomial table of "
+                                        "s2 2^(1-nu)/Gamma(nu) u^nu K_nu(u), 64 segments per "
+                                        "binade (csrc/vgp_ktab.cuh)"}
     if not args.no_cpu_baseline:
         ordered = data.permute(plan.permutation)
         base, parity = cpu_baseline(args, ordered, plan.neighbors.neighbors, res)

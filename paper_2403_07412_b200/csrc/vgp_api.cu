@@ -261,11 +261,9 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
         : ws3_c ? 8
         : (ws3_n ? 7
                  : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
-    const bool ws4_ok = p->m >= 8;
     const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3) && fast_n) || (v == 7 && ws3_n) ||
                     (v == 4 && fast_c) || (v == 8 && ws3_c) || (v == 11 && big_n) || (v == 12 && big_c) ||
-                    (v == 13 && tiny) || (v == 14 && fast_c && ws4_ok) ||
-                    (v == 15 && fast_n && ws4_ok) || (v == 16 && fast_c && ws4_ok);
+                    (v == 13 && tiny);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (p->timing) {
@@ -282,8 +280,6 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
       if (v <= 6 || v >= 9 && v <= 10) return cudaErrorNotSupported;  // retired variants
       if (v <= 8) return launch_loglik_ws3(*p, cp, lo, hi, s, v == 8);
       if (v == 13) return launch_loglik_tiny(*p, cp, lo, hi, s);
-      if (v == 16) return launch_loglik_grp(*p, cp, lo, hi, s);
-      if (v >= 14) return launch_loglik_ws4(*p, cp, lo, hi, s, v == 14);
       return launch_loglik_big(*p, cp, lo, hi, s, v == 12);
     };
     const int64_t count = e_hi - e_lo;
@@ -1081,7 +1077,7 @@ int vgp_plan_kernel_time(vgp_plan* plan, double* ms, int64_t* launches) {
 }
 
 int vgp_plan_set_variant(vgp_plan* plan, int variant) {
-  if (!plan || variant < -1 || variant > 16) return fail(VGP_E_INVALID, "bad variant");
+  if (!plan || variant < -1 || variant > 13) return fail(VGP_E_INVALID, "bad variant");
   // -1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
   // 3 warp-specialised DMMA, 4 warp-specialised streaming the distance cache
   plan->p.force_variant = variant;

@@ -178,13 +178,6 @@ cudaError_t launch_loglik_big(const Plan& p, const CovParams& cp, int64_t e_lo, 
                               cudaStream_t stream, bool cache);
 // Scheduler-aware layout: one worker warp per SM sub-partition serving the
 // two blocks whose chain warps share that sub-partition (vgp_ws3_kernel.cuh).
-// Split-scheduler variant: chain + generation warps on schedulers 0, 1,
-// DMMA update warps on 2, 3 (vgp_ws4_kernel.cuh); 8 <= m, m + 2 <= 64.
-cudaError_t launch_loglik_ws4(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                              cudaStream_t stream, bool cache);
-// Lock-step group kernel (vgp_grp_kernel.cuh): 8 <= m, m + 2 <= 64, distance cache.
-cudaError_t launch_loglik_grp(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                              cudaStream_t stream);
 // closed forms or general nu (table) with m + 2 <= 64
 bool ws3_supported(int m, int kind);
 cudaError_t launch_loglik_ws3(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,

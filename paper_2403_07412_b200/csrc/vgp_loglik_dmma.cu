@@ -59,36 +59,6 @@ cudaError_t launch_loglik_ws3(const Plan& p, const CovParams& cp, int64_t e_lo, 
   }
 }
 
-cudaError_t launch_ws4_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
-cudaError_t launch_ws4_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
-cudaError_t launch_ws4_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
-
-cudaError_t launch_loglik_ws4(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                              cudaStream_t stream, bool cache) {
-  if (!dmma_supported(p.m, cp.kind) || p.m < 8) return cudaErrorNotSupported;
-  if (e_hi <= e_lo) return cudaSuccess;
-  switch (cp.kind) {
-    case kMatern05: return launch_ws4_kMatern05(p, cp, e_lo, e_hi, stream, cache);
-    case kMatern15: return launch_ws4_kMatern15(p, cp, e_lo, e_hi, stream, cache);
-    default: return launch_ws4_kMatern25(p, cp, e_lo, e_hi, stream, cache);
-  }
-}
-
-cudaError_t launch_grp_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
-cudaError_t launch_grp_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
-cudaError_t launch_grp_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
-
-cudaError_t launch_loglik_grp(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                              cudaStream_t stream) {
-  if (!dmma_supported(p.m, cp.kind) || p.m < 8) return cudaErrorNotSupported;
-  if (e_hi <= e_lo) return cudaSuccess;
-  switch (cp.kind) {
-    case kMatern05: return launch_grp_kMatern05(p, cp, e_lo, e_hi, stream);
-    case kMatern15: return launch_grp_kMatern15(p, cp, e_lo, e_hi, stream);
-    default: return launch_grp_kMatern25(p, cp, e_lo, e_hi, stream);
-  }
-}
-
 bool dmma_supported(int m, int kind) {
   return m >= 1 && m + 2 <= 64 && (kind == kMatern05 || kind == kMatern15 || kind == kMatern25);
 }

@@ -200,6 +200,23 @@ def mle_free_nu_case(name, n, m, nu_true, beta_true, init, seed, clustered=False
          mle_seconds=dt)
 
 
+def sphere_large_cases():
+    """Great-circle kNN at scale (glibc-sin keys, vg/geo.py:266-292): the table
+    digest of the reference on 40,000 global points and on 30,000 points in
+    a 2-degree patch (dense, many near-ties), random ordering."""
+    gc = geo.GreatCircle()
+    parallel.set_num_threads(os.cpu_count() or 1)
+    for name, n, m, lon, lat, seed in [("knn_sphere_big_global", 40000, 30, (-180, 180), (-80, 80), 51),
+                                       ("knn_sphere_big_patch", 30000, 20, (10, 12), (45, 47), 52)]:
+        rng = np.random.default_rng(seed)
+        locs = np.column_stack([rng.uniform(*lon, n), rng.uniform(*lat, n)])
+        ordered = geo.Dataset(locs, np.zeros(n), gc).permute(geo.random_ordering(n, 0))
+        t0 = time.perf_counter()
+        t = geo.nearest_neighbors(ordered, m).neighbors
+        print(f"{name}: {time.perf_counter() - t0:.1f}s")
+        save(name, locs=ordered.locations, m=m, table_sha256=table_digest(t), table_head=t[:500])
+
+
 def mle_cases():
     mle_free_nu_case("mle_freenu_n2000_m20_clustered", 2000, 20, 0.8, 0.05, (0.5, 0.1, 1.0), 601,
                      clustered=True)
@@ -336,6 +353,8 @@ def main():
         kl_cases()
     if args.only == "mle":
         mle_cases()
+    if args.only == "sphere_large":
+        sphere_large_cases()
     if args.only in ("", "c1"):
         c1_case(args.with_mle)
 
