@@ -24,7 +24,10 @@ def main(rep, blocks=None, out_json=None):
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
     summary = {k: raw.get(k) for k in keys if k in raw}
     for k in hdr:
         if "pipe_fp64" in k and "pct" in k:
