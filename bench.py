@@ -340,8 +340,8 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-VARIANT_NAMES = {0: "generic", 1: "warp-dmma-allreg", 2: "warp-dmma-grouped",
-                 3: "warp-specialised", 4: "warp-specialised+dcache", 7: "ws-scheduler-aware",
+VARIANT_NAMES = {0: "generic", 1: "warp-dmma-allreg", 4: "warp-specialised+dcache",
+                 7: "ws-scheduler-aware",
                  8: "ws-scheduler-aware+dcache", 11: "large-m-cta", 12: "large-m-cta+dcache",
                  13: "thread-per-block"}
 
@@ -464,6 +464,11 @@ def run_ours_multi(args, rank, world):
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     vg._native.set_device(local)
+    # communicator lines (nranks, NVLS/ring choice) on stderr, so a scaling run
+    # records what NCCL built; stdout stays the one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     locs = synthetic(args.n, kind=args.locations)
     t0 = time.perf_counter()

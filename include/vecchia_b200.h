@@ -243,13 +243,14 @@ int vgp_plan_info(const vgp_plan* plan, int64_t* info);
 /* Force a kernel variant — testing / benchmarking aid.  -1 auto (by m, for
  * closed-form Matern: 13 for m <= 12 (Euclidean), 1 for m + 2 <= 24, 4 for
  * m + 2 <= 56, 8 for m + 2 <= 64 — cached variants when the plan has a
- * distance cache; 11 / 12 for larger m and for general nu / power
- * exponential; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
- * 2 grouped warp-DMMA, 3/4 warp-specialised, 7/8 scheduler-aware
- * warp-specialised (5, 6, 9, 10 are retired experiments returning
- * VGP_E_UNSUPPORTED), 11/12 the CTA-per-block large-m DMMA kernel (any m,
- * every family), 13 thread-per-block (m <= 12, closed-form Matern,
- * Euclidean); even numbers 4..12 stream the plan's distance cache. */
+ * distance cache; general-nu Matern with m + 2 <= 64: 8 (7 without a cache),
+ * covariances from the per-evaluation table; 11 / 12 for larger m and for
+ * power exponential; 0 otherwise), 0 generic, 1 all-register warp-DMMA,
+ * 4 warp-specialised pair + distance cache, 7/8 scheduler-aware
+ * warp-specialised (8: + distance cache), 11/12 the CTA-per-block large-m
+ * DMMA kernel (any m, every family; 12: + distance cache), 13
+ * thread-per-block (m <= 12, closed-form Matern, Euclidean).  2, 3, 5, 6,
+ * 9, 10 are retired experiments (VGP_E_UNSUPPORTED). */
 int vgp_plan_set_variant(vgp_plan* plan, int variant);
 
 /* CUDA stream (cudaStream_t) the plan launches on, for event timing. */

@@ -1,0 +1,145 @@
+"""The two reference CLI entry points that drive the hot path, on the B200
+(SURVEY.md §8(f) row 4): ``bench`` (phase-split timing and the flop model,
+vg/cli.py:241-285) and ``likelihood`` (vg/cli.py:133-150), with the same
+flags and JSON keys, so the reference's acceptance criteria 8 and 9
+(pkg/tests/test_acceptance.py:217-286) can run against this backend.
+
+    python -m paper_2403_07412_b200.cli bench --n 200000 --m 30 --reps 3
+    python -m paper_2403_07412_b200.cli likelihood --input d.csv --m 30
+
+``bench`` times the reference's three stages on the device (``assemble`` ->
+``vgp_assemble``, ``_numeric_stage`` -> batched POTRF/TRSV/dot kernels,
+``_reduction_stage``) and, beside them, the fused single-kernel evaluation
+the package's ``vecchia_loglik`` runs (``fused_eval_seconds``).  The rest of
+the reference CLI (CSV generation, KL sweeps, estimation, kriging front
+ends) is outside this build's scope.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from statistics import median
+
+import numpy as np
+
+from . import errors, exact, geo, kernels, vecchia
+
+
+def _spec(args) -> kernels.KernelSpec:
+    family = "power_exponential" if args.kernel == "powexp" else args.kernel
+    return kernels.KernelSpec(family, kernels.KernelParams(args.sigma2, args.beta, args.nu))
+
+
+def _read_csv(path: str, metric) -> geo.Dataset:
+    """`x,y,value` (or `lon,lat,value` for gcd) rows, header first (vg/cli.py:54-83)."""
+    want = ["lon", "lat", "value"] if isinstance(metric, geo.GreatCircle) else ["x", "y", "value"]
+    with open(path, encoding="utf-8") as fh:
+        header = fh.readline().strip().split(",")
+        if [h.strip() for h in header] != want:
+            raise ValueError(f"{path} line 1: expected header '{','.join(want)}'")
+        rows = np.loadtxt(fh, delimiter=",", ndmin=2)
+    return geo.Dataset(rows[:, :2], rows[:, 2], metric)
+
+
+def cmd_bench(args) -> dict:
+    if not (1 <= args.m < args.n):
+        raise ValueError(f"need 1 <= m < n, got m={args.m}, n={args.n}")
+    spec = _spec(args)
+    loc_seed, obs_seed = np.random.SeedSequence(args.seed).spawn(2)
+    data = geo.Dataset(np.random.default_rng(loc_seed).random((args.n, 2)),
+                       np.random.default_rng(obs_seed).standard_normal(args.n))
+    plan = vecchia.make_plan(data, args.m, args.ordering, args.seed)
+    ordered = data.permute(plan.permutation)
+    phases = {"assembly": [], "factorization_solves": [], "reduction": []}
+    fused = []
+    ws = None
+    loglik = None
+    for rep in range(args.reps + 1):  # rep 0 warms up (allocation, first touch)
+        t0 = time.perf_counter()
+        ws = vecchia.assemble(ordered, plan, spec, out=ws)
+        t1 = time.perf_counter()
+        lower, mu_p, sig_p = vecchia._numeric_stage(ws)
+        t2 = time.perf_counter()
+        res = vecchia._reduction_stage(ws, ordered.observations, plan.m, lower, mu_p, sig_p)
+        t3 = time.perf_counter()
+        total = vecchia.vecchia_loglik(data, plan, spec).total
+        t4 = time.perf_counter()
+        if rep:
+            for k, v in zip(phases, (t1 - t0, t2 - t1, t3 - t2)):
+                phases[k].append(v)
+            fused.append(t4 - t3)
+            loglik = res.total
+    med = {k: median(v) for k, v in phases.items()}
+    med["total"] = med["assembly"] + med["factorization_solves"] + med["reduction"]
+    flops = vecchia.flop_count(args.n, args.m)
+    return {"n": args.n, "m": args.m, "reps": args.reps, "wall_time_seconds": med,
+            "model_flops": flops, "achieved_gflops": flops / med["factorization_solves"] / 1e9,
+            "loglik": loglik, "fused_eval_seconds": median(fused), "fused_loglik": total,
+            "backend": "b200"}
+
+
+def cmd_likelihood(args) -> dict:
+    metric = geo.GreatCircle(radius=args.radius) if args.metric == "gcd" else geo.Euclidean()
+    data = _read_csv(args.input, metric)
+    if not (1 <= args.m < data.n):
+        raise ValueError(f"need 1 <= m < n, got m={args.m}, n={data.n}")
+    spec = _spec(args)
+    plan = vecchia.make_plan(data, args.m, args.ordering, args.seed)
+    out = {"n": data.n, "m": args.m, "ordering": args.ordering,
+           "vecchia_ll": vecchia.vecchia_loglik(data, plan, spec).total}
+    if args.with_exact:
+        ex = exact.exact_loglik(data, spec, max_n=args.max_dense_n)
+        out.update(exact_ll=ex, abs_diff=abs(out["vecchia_ll"] - ex))
+    return out
+
+
+def parser() -> argparse.ArgumentParser:
+    ap = argparse.ArgumentParser(prog="vecchia-b200")
+    sub = ap.add_subparsers(dest="command", required=True)
+
+    def kernel_args(p):
+        p.add_argument("--kernel", choices=["matern", "powexp"], default="matern")
+        p.add_argument("--sigma2", type=float, default=1.0)
+        p.add_argument("--beta", type=float, default=0.1)
+        p.add_argument("--nu", type=float, default=0.5)
+        p.add_argument("--threads", type=int, default=1, help="accepted; the GPU ignores it")
+
+    b = sub.add_parser("bench")
+    b.add_argument("--n", type=int, required=True)
+    b.add_argument("--m", type=int, required=True)
+    b.add_argument("--reps", type=int, default=3)
+    b.add_argument("--seed", type=int, default=0)
+    b.add_argument("--ordering", choices=["random", "morton"], default="random")
+    kernel_args(b)
+    b.set_defaults(func=cmd_bench)
+
+    lk = sub.add_parser("likelihood")
+    lk.add_argument("--input", required=True)
+    lk.add_argument("--m", type=int, required=True)
+    lk.add_argument("--ordering", choices=["random", "morton"], default="random")
+    lk.add_argument("--seed", type=int, default=0)
+    lk.add_argument("--with-exact", action="store_true")
+    lk.add_argument("--max-dense-n", type=int, default=exact.DENSE_GUARD_DEFAULT)
+    lk.add_argument("--metric", choices=["euclidean", "gcd"], default="euclidean")
+    lk.add_argument("--radius", type=float, default=geo.EARTH_RADIUS_KM)
+    kernel_args(lk)
+    lk.set_defaults(func=cmd_likelihood)
+    return ap
+
+
+def main(argv=None) -> int:
+    args = parser().parse_args(argv)
+    try:
+        payload = args.func(args)
+    except (errors.VecchiaGPError, ValueError, OSError) as exc:
+        sys.stderr.write(f"error: {exc}\n")
+        return 2
+    sys.stdout.write(json.dumps(payload, indent=2) + "\n")
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

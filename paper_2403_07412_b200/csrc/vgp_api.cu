@@ -261,7 +261,9 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
         : ws3_c ? 8
         : (ws3_n ? 7
                  : (big_c && big_prefer_cache ? 12 : (big_n ? 11 : (big_c ? 12 : 0))));
-    const bool ok = v == 0 || ((v == 1 || v == 2 || v == 3) && fast_n) || (v == 7 && ws3_n) ||
+    // (2 grouped warp-DMMA and 3 uncached warp-specialised pair: retired in
+    // round 2 — never auto-selected)
+    const bool ok = v == 0 || (v == 1 && fast_n) || (v == 7 && ws3_n) ||
                     (v == 4 && fast_c) || (v == 8 && ws3_c) || (v == 11 && big_n) || (v == 12 && big_c) ||
                     (v == 13 && tiny);
     if (!ok) return fail(VGP_E_UNSUPPORTED, "kernel variant does not cover this plan (m, kernel, metric, cache)");
@@ -275,8 +277,7 @@ int launch_eval(Plan* p, const CovParams& cp, bool want_total, const HostOut* ou
     auto main_kernel = [&](int64_t lo, int64_t hi) -> cudaError_t {
       if (v == 0) return launch_loglik_generic(*p, cp, lo, hi, s);
       if (v == 1) return launch_loglik_dmma(*p, cp, lo, hi, s);
-      if (v == 2) return launch_loglik_ll(*p, cp, lo, hi, s, false);
-      if (v <= 4) return launch_loglik_ws(*p, cp, lo, hi, s, v == 4);
+      if (v == 4) return launch_loglik_ws(*p, cp, lo, hi, s, true);
       if (v <= 6 || v >= 9 && v <= 10) return cudaErrorNotSupported;  // retired variants
       if (v <= 8) return launch_loglik_ws3(*p, cp, lo, hi, s, v == 8);
       if (v == 13) return launch_loglik_tiny(*p, cp, lo, hi, s);

@@ -160,10 +160,6 @@ cudaError_t launch_loglik_generic(const Plan& p, const CovParams& cp, int64_t e_
 cudaError_t launch_loglik_dmma(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                                cudaStream_t stream);
 bool dmma_supported(int m, int kind);
-// Grouped (register-light) warp-DMMA kernel, same coverage (distances from
-// coordinates; `cache` must be false: the cache is laid out for ws).
-cudaError_t launch_loglik_ll(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                             cudaStream_t stream, bool cache);
 // Warp-specialised DMMA kernel (chain + worker warp per block), same
 // coverage; `cache` streams the plan's distance cache (vgp_dcache.cu).
 cudaError_t launch_loglik_ws(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,

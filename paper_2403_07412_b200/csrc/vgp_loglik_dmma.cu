@@ -7,21 +7,6 @@ cudaError_t launch_dmma_kMatern05(const Plan&, const CovParams&, int64_t, int64_
 cudaError_t launch_dmma_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
 cudaError_t launch_dmma_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t);
 
-cudaError_t launch_ll_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
-cudaError_t launch_ll_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
-cudaError_t launch_ll_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
-
-cudaError_t launch_loglik_ll(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                             cudaStream_t stream, bool cache) {
-  if (!dmma_supported(p.m, cp.kind)) return cudaErrorNotSupported;
-  if (e_hi <= e_lo) return cudaSuccess;
-  switch (cp.kind) {
-    case kMatern05: return launch_ll_kMatern05(p, cp, e_lo, e_hi, stream, cache);
-    case kMatern15: return launch_ll_kMatern15(p, cp, e_lo, e_hi, stream, cache);
-    default: return launch_ll_kMatern25(p, cp, e_lo, e_hi, stream, cache);
-  }
-}
-
 cudaError_t launch_ws_kMatern05(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
 cudaError_t launch_ws_kMatern15(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);
 cudaError_t launch_ws_kMatern25(const Plan&, const CovParams&, int64_t, int64_t, cudaStream_t, bool);

@@ -201,9 +201,10 @@ class DevicePlan:
         return int(self.info()[6])
 
     def set_variant(self, variant: int) -> None:
-        """-1 auto, 0 generic, 1 all-register warp-DMMA, 2 grouped warp-DMMA,
-        3 warp-specialised DMMA (distances from coordinates), 4 warp-specialised
-        streaming the distance cache (testing aid)."""
+        """Force a kernel variant (testing aid; see vgp_plan_set_variant in
+        include/vecchia_b200.h): -1 auto, 0 generic, 1 all-register warp-DMMA,
+        4 warp-specialised + distance cache, 7/8 scheduler-aware, 11/12
+        CTA-per-block, 13 thread-per-block."""
         N.check(N.lib.vgp_plan_set_variant(self.handle, int(variant)))
 
     def set_data(self, dataset: geo.Dataset) -> None:

@@ -1,0 +1,68 @@
+"""GPU: the reference's acceptance criteria 8 and 9 (pkg/tests/test_acceptance.py:217-286)
+against this backend's CLI entry points (paper_2403_07412_b200.cli)."""
+
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cli():
+    import paper_2403_07412_b200 as vg
+    from paper_2403_07412_b200 import cli
+
+    if vg._native.device_count() == 0:
+        pytest.fail("GPU tests need a CUDA device: the B200 path has no CPU fallback")
+    return cli
+
+
+def _run(cli, capsys, *argv):
+    code = cli.main(list(argv))
+    return code, capsys.readouterr().out
+
+
+def test_criterion_8_complexity_model(cli, capsys):
+    """Wall time grows linearly in n at fixed m (ratios in [1.5, 2.5]); the
+    flop model is exactly (n - m + 1)(m^3/3 + 2 m^2 + 4 m) (vg/vecchia.py:241-251)."""
+    from paper_2403_07412_b200 import vecchia
+
+    totals = {}
+    for n in (50_000, 100_000, 200_000):
+        code, out = _run(cli, capsys, "bench", "--n", str(n), "--m", "30", "--reps", "3", "--seed", "8")
+        assert code == 0
+        payload = json.loads(out)
+        totals[n] = payload["wall_time_seconds"]["total"]
+        m = 30
+        expected = float(n - m + 1) * (m**3 / 3.0 + 2.0 * m**2 + 4.0 * m)
+        assert payload["model_flops"] == expected == vecchia.flop_count(n, m)
+        # the staged and fused evaluations are the same likelihood
+        assert abs(payload["loglik"] - payload["fused_loglik"]) <= 1e-9 * abs(payload["fused_loglik"])
+    r1 = totals[100_000] / totals[50_000]
+    r2 = totals[200_000] / totals[100_000]
+    assert 1.5 <= r1 <= 2.5 and 1.5 <= r2 <= 2.5, (r1, r2)
+
+
+def test_criterion_9_determinism(cli, capsys, tmp_path):
+    """Reruns under different --threads emit identical bytes (timings exempt)."""
+    rng = np.random.default_rng(9)
+    locs = rng.random((80, 2))
+    vals = rng.standard_normal(80)
+    path = tmp_path / "d.csv"
+    path.write_text("x,y,value\n" + "".join(f"{format(a, '.17g')},{format(b, '.17g')},{format(v, '.17g')}\n"
+                                             for (a, b), v in zip(locs, vals)))
+    outs = [_run(cli, capsys, "likelihood", "--input", str(path), "--m", "12", "--with-exact",
+                 "--threads", t) for t in ("1", "3")]
+    assert outs[0][0] == outs[1][0] == 0 and outs[0][1] == outs[1][1]
+    benches = []
+    for t in ("1", "3"):
+        code, out = _run(cli, capsys, "bench", "--n", "2000", "--m", "10", "--reps", "2", "--seed", "3",
+                         "--threads", t)
+        assert code == 0
+        j = json.loads(out)
+        assert all(v > 0.0 for v in j.pop("wall_time_seconds").values())
+        assert np.isfinite(j.pop("achieved_gflops")) and j.pop("fused_eval_seconds") > 0
+        benches.append(j)
+    assert benches[0] == benches[1]

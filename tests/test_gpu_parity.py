@@ -102,7 +102,7 @@ def _plan_from_golden(vg, z):
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("ll_") if "fail" not in n])
-@pytest.mark.parametrize("variant", [-1, 0, 1, 2, 3, 4, 7, 8, 11, 12, 13])
+@pytest.mark.parametrize("variant", [-1, 0, 1, 4, 7, 8, 11, 12, 13])
 def test_loglik_vs_reference_golden(vg, name, variant):
     z = load(name)
     data, plan, spec = _plan_from_golden(vg, z)
@@ -113,9 +113,9 @@ def test_loglik_vs_reference_golden(vg, name, variant):
     gen3 = str(z["family"]) == "matern" and not closed and int(z["m"]) + 2 <= 64
     if variant in (7, 8) and not (fast or gen3):
         pytest.skip("scheduler-aware kernel: m + 2 <= 64 Matern")
-    if variant in (1, 2, 3, 4) and not fast:
+    if variant in (1, 4) and not fast:
         pytest.skip("warp-DMMA variants cover m + 2 <= 64 closed-form Matern only")
-    if variant in (1, 2, 3, 7, 11) and not plane:
+    if variant in (1, 7, 11) and not plane:
         pytest.skip("distances computed in the kernel are Euclidean (great circle: cached variants)")
     cache = not plane or int(z["m"]) + 2 <= 64
     if variant == 12 and not cache:
@@ -327,8 +327,6 @@ def test_distance_cache_is_bit_identical(vg, name):
     dp.set_variant(4)  # warp-specialised kernel streaming the cache
     a = vg.vecchia_loglik(data, plan, spec)
     cached = dp.info()[8] == 1
-    dp.set_variant(3)  # same warp-specialised kernel, distances from coordinates
-    b = vg.vecchia_loglik(data, plan, spec)
     dp.set_variant(8)
     f = vg.vecchia_loglik(data, plan, spec)
     dp.set_variant(7)

@@ -17,8 +17,8 @@ def page(rep, name, extra=()):
 
 def main(rep, blocks=None, out_json=None):
     rows = page(rep, "raw")
-    hdr, vals = rows[0], rows[2]
-    raw = dict(zip(hdr, vals))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    raw = {k: (f"{v} {u}".strip() if u else v) for k, u, v in zip(hdr, units, vals)}
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__inst_executed_pipe_fp64.sum", "smsp__inst_executed.sum",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
