@@ -315,10 +315,16 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
                 const double nxt = fma(-a[j], a[j], a[j + 1]);
                 piv = shfl(nxt, j + 1);
               }
+              // column j of L_cc straight into its published slot (Lt[8 j + row])
+              // and back to every lane with broadcast LDS.128: 4 loads instead
+              // of 14 32-bit shuffles per pivot on the block's critical path
+              if (lane < 8) Lt[8 * j + lane] = a[j];
+              __syncwarp();
 #pragma unroll
-              for (int jp = j + 1; jp < 8; ++jp) {
-                const double lc = shfl(a[j], jp);  // L[R0 + jp][R0 + j]
-                a[jp] = fma(-a[j], lc, a[jp]);
+              for (int x = (j + 1) & ~1; x < 8; x += 2) {
+                const double2 lv = ld2(Lt + 8 * j + x);  // L[R0 + x][R0 + j], L[R0 + x + 1][R0 + j]
+                if (x >= j + 1) a[x] = fma(-a[j], lv.x, a[x]);
+                if (x + 1 >= j + 1) a[x + 1] = fma(-a[j], lv.y, a[x + 1]);
               }
             }
           }
@@ -334,9 +340,7 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
           fj = R0 + (bad ? __ffs(bad) - 1 : jmax - 1);
         }
         if (!lastc) {
-#pragma unroll
-          for (int k = 0; k < 7; ++k)
-            if (lane > k && lane < 8) Lt[8 * k + lane] = a[k];
+          // (L_cc itself was published column by column in the pivot loop)
           if (lane == 0) {
             st2(Iv, iv[0], iv[1]);
             st2(Iv + 2, iv[2], iv[3]);

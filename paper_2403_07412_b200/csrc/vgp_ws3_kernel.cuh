@@ -77,10 +77,10 @@ __device__ __forceinline__ double cov_gen(double d, double inv_beta, const doubl
 
 struct SlotLayout {
   int tiles;   // doubles of the tile triangle (= cache stride)
-  int stride;  // tiles | S (2 tiles) | O (P) | XY (2P) | yt (2) | mbarrier (2)
+  int stride;  // tiles | S (2 tiles) | O (P) | XY (2P) | yt (2) | mbarrier (2) | Lc (2 x 8)
 };
 __host__ __device__ constexpr SlotLayout slot_layout(int nt) {
-  return SlotLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2};
+  return SlotLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2 + 16};
 }
 
 template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false>
@@ -106,6 +106,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   auto XYb = [&](int s) { return reinterpret_cast<double2*>(Ob(s) + P); };
   auto Yb = [&](int s) { return Ob(s) + 3 * P; };  // [parity] target observation
   auto MBb = [&](int s) { return reinterpret_cast<uint64_t*>(Ob(s) + 3 * P + 2); };
+  auto Lcb = [&](int s) { return Ob(s) + 3 * P + 4; };  // [pivot parity][8] column of L_cc
   // named barriers (ids 0..15; id 0 is free again after the setup __syncthreads):
   // 2s = tile column staged (worker -> chain), 2s + 1 = L written (chain -> worker)
 
@@ -338,12 +339,26 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                   const double nxt = fma(-a[0][j], a[0][j], a[0][j + 1]);
                   piv = shfl(nxt, j + 1);
                 }
+                // column j of L_cc to every lane: the diagonal-tile lanes store
+                // it, every lane reads it back with broadcast LDS.128 (4
+                // instructions instead of 14 32-bit shuffles; double-buffered
+                // by pivot parity, so one __syncwarp per pivot orders both
+                // the reads after the store and the next-but-one overwrite)
+                double* Lc = Lcb(s) + 8 * (j & 1);
+                if (lane < 8) Lc[lane] = a[0][j];
+                __syncwarp();
+                double lcv[8];
+#pragma unroll
+                for (int x = (j + 1) & ~1; x < 8; x += 2) {
+                  const double2 v = ld2(Lc + x);
+                  lcv[x] = v.x;
+                  lcv[x + 1] = v.y;
+                }
 #pragma unroll
                 for (int jp = j + 1; jp < 8; ++jp) {
-                  const double lc = shfl(a[0][j], jp);  // L[R0 + jp][R0 + j]
 #pragma unroll
                   for (int rr = 0; rr < kMaxRows; ++rr)
-                    if (rr * 32 < NR) a[rr][jp] = fma(-a[rr][j], lc, a[rr][jp]);
+                    if (rr * 32 < NR) a[rr][jp] = fma(-a[rr][j], lcv[jp], a[rr][jp]);
                 }
               }
             }
