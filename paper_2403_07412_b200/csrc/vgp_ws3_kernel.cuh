@@ -77,13 +77,16 @@ __device__ __forceinline__ double cov_gen(double d, double inv_beta, const doubl
 
 struct SlotLayout {
   int tiles;   // doubles of the tile triangle (= cache stride)
-  int stride;  // tiles | S (2 tiles) | O (P) | XY (2P) | yt (2) | mbarrier (2) | Lc (2 x 8)
+  int stride;  // tiles | S (2 tiles) | O (P) | XY (2P) | yt (2) | mbarrier (2) | Lc (2 x 8) | gen mbarriers (2)
 };
 __host__ __device__ constexpr SlotLayout slot_layout(int nt) {
-  return SlotLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2 + 16};
+  return SlotLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2 + 16 + 2};
 }
 
-template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false>
+// CG: the chain warps generate the covariance (in place over the cached
+// distances, one column ahead, in the time they otherwise wait for their
+// worker); the workers only load it and run the DMMA updates.
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false>
 __global__ void __launch_bounds__(kThreads, 1)
 loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
                   int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
@@ -107,11 +110,16 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   auto Yb = [&](int s) { return Ob(s) + 3 * P; };  // [parity] target observation
   auto MBb = [&](int s) { return reinterpret_cast<uint64_t*>(Ob(s) + 3 * P + 2); };
   auto Lcb = [&](int s) { return Ob(s) + 3 * P + 4; };  // [pivot parity][8] column of L_cc
+  auto GBb = [&](int s) { return reinterpret_cast<uint64_t*>(Ob(s) + 3 * P + 20); };  // CG: [2] column generated
   // named barriers (ids 0..15; id 0 is free again after the setup __syncthreads):
   // 2s = tile column staged (worker -> chain), 2s + 1 = L written (chain -> worker)
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) smem[i] = s2 * kExp2Table[i];
   if (CACHE && warp < kSlots && lane == 0) mbar_init(MBb(warp));
+  if (CG && warp < kSlots && lane < 2) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(dmma::smem_u32(GBb(warp) + lane)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   const double* tab = smem;
 
@@ -145,14 +153,24 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
       pf1[h] = pf0[h];
       const int64_t e = e0 + sl[h];
       if (e < e_hi) {
-        if (CACHE && lane == 0)
+        if (!CG && CACHE && lane == 0)
           bulk_load(Tb(sl[h]), dcache + (e - 1 - rest_lo) * cstride, cbytes, MBb(sl[h]));
         pf0[h] = slot_point(slot_index(e, lane));
         if (P > 32) pf1[h] = slot_point(slot_index(e, lane + 32));
+        if (CG) {
+          // the chain generates from O: stage it, then the distances (the
+          // mbarrier's release by lane 0 after __syncwarp covers both)
+          double* O = Ob(sl[h]);
+          if (lane < P) O[lane] = lane < m ? pf0[h].z : 0.0;
+          if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1[h].z : 0.0;
+          __syncwarp();
+          if (lane == 0) bulk_load(Tb(sl[h]), dcache + (e - 1 - rest_lo) * cstride, cbytes, MBb(sl[h]));
+        }
       }
     }
     int par = 0;
     bool first = true;
+    uint32_t gcnt[2] = {0, 0};  // CG: generated columns consumed per slot
     for (int64_t base = e0; base + sl[0] < e_hi; base += stride, par ^= 1, first = false, ++tblk) {
       bool act[2];
 #pragma unroll
@@ -164,8 +182,10 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
         mark(s, 1, 0);
         double* O = Ob(s);
         double2* XY = XYb(s);
-        if (lane < P) O[lane] = lane < m ? pf0[h].z : 0.0;
-        if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1[h].z : 0.0;
+        if (!CG) {
+          if (lane < P) O[lane] = lane < m ? pf0[h].z : 0.0;
+          if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1[h].z : 0.0;
+        }
         if (!CACHE) {
           if (lane < P) XY[lane] = make_double2(pf0[h].x, pf0[h].y);
           if (P > 32 && lane + 32 < P) XY[lane + 32] = make_double2(pf1[h].x, pf1[h].y);
@@ -180,7 +200,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (CACHE && act[h]) {
+        if (!CG && CACHE && act[h]) {
           mbar_wait(MBb(sl[h]), phase[h]);
           phase[h] ^= 1;
         }
@@ -208,9 +228,22 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             }
             // ---- generate tile column c: entries (8I + r, 8c + 2q + h)
             double acc[NT][2];
+            if (CG) {
+              // generated by the chain (column c of this slot's block)
+              mbar_wait(GBb(s) + (gcnt[h] & 1), (gcnt[h] >> 1) & 1);
+              ++gcnt[h];
+#pragma unroll
+              for (int I = 0; I < NT; ++I) {
+                if (I >= c) {
+                  const double2 v = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
+                  acc[I][0] = v.x;
+                  acc[I][1] = v.y;
+                }
+              }
+            }
 #pragma unroll
             for (int I = 0; I < NT; ++I) {
-              if (I >= c) {
+              if (!CG && I >= c) {
                 const int i = 8 * I + r;
                 double v0, v1;
                 if (CACHE) {
@@ -262,7 +295,13 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             }
             if (lastc) {
               // T is no longer read for this block (the last panel runs from
-              // S): stream in the next block's distances
+              // S): stream in the next block's distances (CG: and its
+              // observations, which the chain generates from)
+              if (CG && en < e_hi) {
+                double* O = Ob(s);
+                if (lane < P) O[lane] = lane < m ? pf0[h].z : 0.0;
+                if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1[h].z : 0.0;
+              }
               __syncwarp();
               if (CACHE && lane == 0 && en < e_hi)
                 bulk_load(T, dcache + (en - 1 - rest_lo) * cstride, cbytes, MBb(s));
@@ -289,8 +328,38 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
     double* T = Tb(s);
     double* S = Sb(s);
     int par = 0;
+    uint32_t dph = 0, gcnt = 0;
+    // CG: generate tile column c in place over the cached distances and
+    // hand it to the worker
+    auto gen_col = [&](const int c) {
+#pragma unroll
+      for (int I = 0; I < NT; ++I) {
+        if (I >= c) {
+          const int i = 8 * I + r;
+          double* tp = T + tidx(I, c, NT) * 64 + chunk_off(r, q);
+          const double2 dv = ld2(tp);
+          double v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx);
+          double v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx);
+          if (I == NT - 1 && i > m) {  // row m+1: yJ (0 from column m on); padding: 0
+            const double2 ov = ld2(Ob(s) + 8 * c + 2 * q);
+            v0 = i == m + 1 ? ov.x : 0.0;
+            v1 = i == m + 1 ? ov.y : 0.0;
+          }
+          st2(tp, v0, v1);
+        }
+      }
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(dmma::smem_u32(GBb(s) + (gcnt & 1)))
+                   : "memory");
+      ++gcnt;
+    };
     for (int64_t e = e0 + s; e < e_hi; e += stride, par ^= 1, ++tblk) {
       int fj = -1;  // first non-positive pivot column
+      if (CG) {
+        mbar_wait(MBb(s), dph);  // this block's distances and observations
+        dph ^= 1;
+        gen_col(0);
+        if (NC > 1) gen_col(1);
+      }
 #pragma unroll
       for (int c = 0; c < NT; ++c) {
         if (c < NC) {
@@ -387,6 +456,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
               }
             }
             bar_arrive(2 * s + 1, 64);
+            if (CG && c + 2 < NC) gen_col(c + 2);
           } else {
             // sigma_new = A[m][m], -mu = A[m+1][m] after m pivots (vg/vecchia.py:186-189, :206)
             const int cs = m - R0;
@@ -420,14 +490,14 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   }
 }
 
-template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false>
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, long long* trace = nullptr) {
   constexpr SlotLayout L = slot_layout(NT);
   const size_t sm = sizeof(double) * ((size_t)kHead + (size_t)kSlots * L.stride);
   static size_t configured[64] = {};
   const int dev = p.device & 63;
-  auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE>;
+  auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE, CG>;
   if (configured[dev] < sm) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
@@ -469,6 +539,11 @@ cudaError_t launch_c(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e
   if (NT == 8 && KIND == kMatern15 && MC == 60 && cache) {
     if (const char* path = std::getenv("VGP_TRACE3")) return launch_traced(p, cp, e_lo, e_hi, stream, path);
   }
+  // general nu: covariance generation (the K_nu table) is the expensive part,
+  // so the chains generate in their idle time (c5: 12.2 -> 15.4 evals/s); for
+  // the closed forms it only lengthens the chains (c2: 115.8 -> 106.2)
+  if (cache && (KIND == kMaternGen || p.tune == 2))
+    return launch<NT, KIND, MC, true, false, true>(p, cp, e_lo, e_hi, stream);
   if (cache) return launch<NT, KIND, MC, true>(p, cp, e_lo, e_hi, stream);
   return launch<NT, KIND, MC, false>(p, cp, e_lo, e_hi, stream);
 }
