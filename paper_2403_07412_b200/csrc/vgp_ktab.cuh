@@ -46,16 +46,19 @@ __device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ 
                                            const CovParams& cp, ExpNeg e_neg) {
   const int hi = __double2hiint(u);
   const int lo = __double2loint(u);
-  const int ex = (hi >> 20) - 1023;
+  const int bex = hi >> 20;  // biased exponent (u >= 0)
   // the diagonal and exact duplicates carry distance 2^-500 (the kernels'
   // sqrt guard) or 0: C(0) = s2 (vg/kernels.py:77-78); genuine near-duplicate
   // distances take the exact path
-  if (ex < kKtabOMin) return u > 1e-90 ? matern_gen_exact(u, cp) : cp.s2;
-  if (ex > kKtabOMax) return 0.0;
-  const int k = (hi >> 14) & (kKtabSeg - 1);
-  const double us = __hiloint2double((hi & 0x000FFFFF) | ((1023 + 7) << 20), lo);  // [128, 256)
-  const double t = us - (double)(129 + 2 * k);
-  const double2* c = reinterpret_cast<const double2*>(ktab + (size_t)((ex - kKtabOMin) * kKtabSeg + k) * 8);
+  if (__builtin_expect(bex < 1023 + kKtabOMin, 0)) return u > 1e-90 ? matern_gen_exact(u, cp) : cp.s2;
+  if (__builtin_expect(bex > 1023 + kKtabOMax, 0)) return 0.0;
+  // segment = (binade, top 6 mantissa bits); t in [-1, 1) from the remaining
+  // 46 mantissa bits: d = 1 + f_low / 64 in [1, 1 + 1/64), t = 128 d - 129
+  // = 2 f_low - 1 (both exact)
+  const int seg = ((hi >> 14) & 0x1FFFF) - ((1023 + kKtabOMin) << 6);
+  const double d = __hiloint2double((hi & 0x3FFF) | 0x3FF00000, lo);
+  const double t = fma(d, 128.0, -129.0);
+  const double2* c = reinterpret_cast<const double2*>(ktab + (size_t)seg * 8);
   const double2 c01 = __ldg(c), c23 = __ldg(c + 1), c45 = __ldg(c + 2), c67 = __ldg(c + 3);
   double p = fma(c67.y, t, c67.x);
   p = fma(p, t, c45.y);
@@ -64,7 +67,8 @@ __device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ 
   p = fma(p, t, c23.x);
   p = fma(p, t, c01.y);
   p = fma(p, t, c01.x);
-  return ex >= 0 ? p * e_neg(u) : cp.s2 - p;
+  if (__builtin_expect(bex >= 1023, 0)) return p * e_neg(u);  // u >= 1: exp-scaled form
+  return cp.s2 - p;
 }
 
 // (re)build the table for cp (kind kMaternGen) into d_ktab (kKtabDoubles)
