@@ -83,9 +83,10 @@ __host__ __device__ constexpr SlotLayout slot_layout(int nt) {
   return SlotLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 2 + 2 + 16 + 2};
 }
 
-// CG: the chain warps generate the covariance (in place over the cached
-// distances, one column ahead, in the time they otherwise wait for their
-// worker); the workers only load it and run the DMMA updates.
+// CG: the chain warps generate half of the covariance tiles (in place over
+// the cached distances, one column ahead, in the time they otherwise wait for
+// their worker); the workers generate the other half and load these.
+__host__ __device__ constexpr bool chain_tile(int I, int c) { return ((I - c) & 1) == 0; }
 template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false>
 __global__ void __launch_bounds__(kThreads, 1)
 loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
@@ -234,7 +235,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
               ++gcnt[h];
 #pragma unroll
               for (int I = 0; I < NT; ++I) {
-                if (I >= c) {
+                if (I >= c && chain_tile(I, c)) {
                   const double2 v = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
                   acc[I][0] = v.x;
                   acc[I][1] = v.y;
@@ -243,7 +244,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             }
 #pragma unroll
             for (int I = 0; I < NT; ++I) {
-              if (!CG && I >= c) {
+              if (I >= c && !(CG && chain_tile(I, c))) {
                 const int i = 8 * I + r;
                 double v0, v1;
                 if (CACHE) {
@@ -334,7 +335,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
     auto gen_col = [&](const int c) {
 #pragma unroll
       for (int I = 0; I < NT; ++I) {
-        if (I >= c) {
+        if (I >= c && chain_tile(I, c)) {
           const int i = 8 * I + r;
           double* tp = T + tidx(I, c, NT) * 64 + chunk_off(r, q);
           const double2 dv = ld2(tp);
