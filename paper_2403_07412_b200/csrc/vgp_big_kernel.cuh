@@ -72,6 +72,17 @@ __host__ __device__ inline int head_doubles(int m, int kind = kMaternGen) {
   return g_offset(kind) + 4 * 8 * ntiles_of(m) + 2;
 }
 
+// Shared-memory tile slots: tile (I, J) is live from its generation (look-ahead
+// at column J - 1) to its last use as L (column I - 1); tiles with disjoint
+// lifetimes share a slot (greedy interval colouring on the host,
+// big_slot_map).  m = 120: 73 slots instead of 136 tiles, 4 CTAs per SM
+// instead of 3.  The global-scratch path keeps the plain triangle.
+constexpr int kMaxSlotTiles = 528;  // NT <= 32
+struct SlotMap {
+  int16_t s[kMaxSlotTiles];
+};
+int big_slot_map(int nt, SlotMap* map);  // returns the slot count
+
 // one 4-row TMA gather of 32-byte point rows into shared memory (tile::gather4)
 __device__ __forceinline__ void gather4(void* dst, const CUtensorMap* map, int r0, int r1, int r2,
                                         int r3, uint64_t* bar) {
@@ -90,7 +101,7 @@ __host__ __device__ inline int64_t tile_doubles(int m) {
 // (vg/kernels.py:75-81).  Not inlined: the kernel evaluates covariances at
 // 2 * kGroup unrolled sites, and eight inlined copies of the Bessel K
 // iteration overflow the instruction cache (profiles/r01_ncu_c5_*.txt).
-__device__ __noinline__ double matern_gen(double d, const CovParams& cp, const double* btab) {
+static __device__ __noinline__ double matern_gen(double d, const CovParams& cp, const double* btab) {
   const double u = d / cp.beta;
   return cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k_tab(cp, u, btab);
 }
@@ -114,14 +125,14 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
   return cov_ref(cp, d);
 }
 
-template <int KIND, bool CACHE, bool GT, int MC = 0>
+template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false>
 __global__ void __launch_bounds__(kThreads, GT ? 3 : 4)
 loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __restrict__ nbr,
                   int m_rt, int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
                   const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch,
-                  const double* __restrict__ ktab) {
+                  const double* __restrict__ ktab, const __grid_constant__ SlotMap smap) {
   // MC > 0: conditioning size fixed at compile time (tile counts and
   // addresses fold to constants)
   const int m = MC > 0 ? MC : m_rt;
@@ -150,7 +161,9 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
   }
   __syncthreads();
   const double* tab = smem;
-  auto tile = [&](int I, int J) -> double* { return T + (size_t)tidx(I, J, NT) * 64; };
+  auto tile = [&](int I, int J) -> double* {
+    return T + (size_t)(SLOTS ? smap.s[tidx(I, J, NT)] : tidx(I, J, NT)) * 64;
+  };
   // block eb's point rows: lane l of warp 1 gathers rows 4l..4l+3 (P / 4 <= 32
   // lanes per pass): neighbours a < m, the target at a = m, row 0 as padding
   const uint32_t gbytes = (uint32_t)(P * sizeof(double4));
@@ -223,14 +236,12 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
           // active tiles of this group (warp-uniform): inactive slots issue no
           // loads and no DMMAs
           const int ng = min(kGroup, (NT - 1 - I0) / nw + 1);
-          // tile (I, k) at colbase(k) + I, colbase(k) = k NT - k (k+1) / 2 (column-major)
-          const double* col = T + chunk_off(r, q);
-          for (int k = 0; k <= kmax; col += (size_t)(NT - k) * 64, ++k) {
-            const double2 b = ld2(col + (size_t)(J - k) * 64);
+          for (int k = 0; k <= kmax; ++k) {
+            const double2 b = ld2(tile(J, k) + chunk_off(r, q));
             double2 a[kGroup];
 #pragma unroll
             for (int g = 0; g < kGroup; ++g)
-              if (g < ng) a[g] = ld2(col + (size_t)(I0 + g * nw - k) * 64);
+              if (g < ng) a[g] = ld2(tile(I0 + g * nw, k) + chunk_off(r, q));
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
@@ -246,12 +257,11 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
     // the last left-looking step of tile column J: reload, apply L of column
     // k, stage (tiles dealt round-robin over all warps)
     auto column_finish = [&](const int J, const int k) {
-      const double* col = T + (size_t)tidx(k, k, NT) * 64 + chunk_off(r, q);
-      const double2 b = ld2(col + (size_t)(J - k) * 64);
+      const double2 b = ld2(tile(J, k) + chunk_off(r, q));
       for (int I = J + warp; I < NT; I += kWarps) {
         double* tp = tile(I, J) + chunk_off(r, q);
         const double2 v = ld2(tp);
-        const double2 a = ld2(col + (size_t)(I - k) * 64);
+        const double2 a = ld2(tile(I, k) + chunk_off(r, q));
         double a0 = v.x, a1 = v.y;
         mma(a0, a1, neg(a.x), b.x);
         mma(a0, a1, neg(a.y), b.y);
@@ -423,23 +433,44 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
   }
 }
 
-inline size_t smem_bytes(int m, bool gt, int kind = kMaternGen) {
-  return sizeof(double) * ((size_t)head_doubles(m, kind) + (gt ? 0 : (size_t)tile_doubles(m)));
+// shared memory per CTA: the plain tile triangle, or (slots) the compacted
+// slot set
+inline size_t smem_bytes(int m, bool gt, int kind = kMaternGen, bool slots = false) {
+  if (gt) return sizeof(double) * (size_t)head_doubles(m, kind);
+  int tiles = (int)(tile_doubles(m) / 64);
+  if (slots) {
+    SlotMap map;
+    tiles = big_slot_map(ntiles_of(m), &map);
+    if (tiles < 0) return (size_t)1 << 40;  // beyond the slot map
+  }
+  return sizeof(double) * ((size_t)head_doubles(m, kind) + (size_t)tiles * 64);
 }
-// tiles in shared memory up to ~200 KB per CTA, else the global scratch
-inline bool use_global_tiles(int m) { return smem_bytes(m, false) > 200 * 1024; }
+inline int ctas_per_sm(size_t bytes) {  // by shared memory (228 KB, 1 KB reserved per CTA), <= 4
+  const size_t per = bytes + 1024;
+  const int n = (int)((size_t)233472 / per);
+  return n < 4 ? n : 4;
+}
+// the slot layout only where it buys resident CTAs (its lookups cost ~6%)
+inline bool use_slots(int m, int kind) {
+  return ctas_per_sm(smem_bytes(m, false, kind, true)) > ctas_per_sm(smem_bytes(m, false, kind, false));
+}
+// tiles in shared memory up to ~200 KB per CTA (compacted when that fits),
+// else the global scratch
+inline bool use_global_tiles(int m) {
+  return smem_bytes(m, false) > 200 * 1024 && smem_bytes(m, false, kMaternGen, true) > 200 * 1024;
+}
 
 // TMA descriptor of the plan's points: a 2-D tensor of n rows x 4 doubles
 // (x, y, obs, 0), one row per box, for tile::gather4
 bool point_map(const double4* pts, int64_t n, CUtensorMap* map);
 
-template <int KIND, bool CACHE, bool GT, int MC = 0>
+template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, double* gscratch, int max_grid) {
   CUtensorMap map;
   if (!point_map(p.d_pts, p.n, &map)) return cudaErrorNotSupported;
-  const size_t sm = smem_bytes(p.m, GT, KIND);
-  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC>;
+  const size_t sm = smem_bytes(p.m, GT, KIND, SLOTS);
+  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC, SLOTS>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (err != cudaSuccess) return err;
   int per_sm = 0;
@@ -450,10 +481,12 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   int64_t cap = (int64_t)p.num_sms * per_sm;
   if (GT && cap > max_grid) cap = max_grid;
   const int grid = (int)(count < cap ? count : cap);
+  SlotMap smap;
+  if (SLOTS) big_slot_map(ntiles_of(p.m), &smap);
   kern<<<grid, kThreads, sm, stream>>>(map, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp,
                                        p.d_rest, p.d_mu, p.d_sig, p.d_fail,
                                        p.d_dcache, p.dcache_stride, gscratch,
-                                       (KIND == kMaternGen && !p.no_ktab) ? p.d_ktab : nullptr);
+                                       (KIND == kMaternGen && !p.no_ktab) ? p.d_ktab : nullptr, smap);
   return cudaGetLastError();
 }
 
@@ -462,16 +495,20 @@ cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_
                         cudaStream_t stream, bool cache, double* gscratch, int max_grid) {
   const bool gt = use_global_tiles(p.m);
   if (gt && !gscratch) return cudaErrorInvalidValue;
+  const bool slots = !gt && (use_slots(p.m, KIND) || smem_bytes(p.m, false, KIND) > 200 * 1024);
   if (cache) {
     // config 5 (m = 60, general nu, streamed distances): compile-time m
     if (p.m == 60 && KIND == kMaternGen) return launch<KIND, true, false, 60>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
-    return gt ? launch<KIND, true, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
-              : launch<KIND, true, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+    if (gt) return launch<KIND, true, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+    return slots ? launch<KIND, true, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
+                 : launch<KIND, true, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
   }
-  // config 4 (m = 120, closed forms, distances from coordinates): compile-time m
-  if (p.m == 120 && KIND <= kMatern25) return launch<KIND, false, false, 120>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
-  return gt ? launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
-            : launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  // config 4 (m = 120, closed forms, distances from coordinates): compile-time
+  // m, slot layout (4 CTAs per SM instead of 3)
+  if (p.m == 120 && KIND <= kMatern25) return launch<KIND, false, false, 120, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  if (gt) return launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  return slots ? launch<KIND, false, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
+               : launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
 }
 
 }  // namespace big
