@@ -126,7 +126,7 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
 }
 
 template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false>
-__global__ void __launch_bounds__(kThreads, GT ? 3 : 4)
+__global__ void __launch_bounds__(kThreads, GT ? 3 : (SLOTS && MC == 120 ? 5 : 4))
 loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __restrict__ nbr,
                   int m_rt, int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
@@ -445,10 +445,10 @@ inline size_t smem_bytes(int m, bool gt, int kind = kMaternGen, bool slots = fal
   }
   return sizeof(double) * ((size_t)head_doubles(m, kind) + (size_t)tiles * 64);
 }
-inline int ctas_per_sm(size_t bytes) {  // by shared memory (228 KB, 1 KB reserved per CTA), <= 4
+inline int ctas_per_sm(size_t bytes, int cap = 4) {  // by shared memory (228 KB, 1 KB reserved per CTA)
   const size_t per = bytes + 1024;
   const int n = (int)((size_t)233472 / per);
-  return n < 4 ? n : 4;
+  return n < cap ? n : cap;
 }
 // the slot layout only where it buys resident CTAs (its lookups cost ~6%)
 inline bool use_slots(int m, int kind) {
