@@ -57,6 +57,7 @@ def cmd_bench(args) -> dict:
     fused = []
     ws = None
     loglik = None
+    vecchia.vecchia_loglik(data, plan, spec)  # warm the device plan and result pool
     for rep in range(args.reps + 1):  # rep 0 warms up (allocation, first touch)
         t0 = time.perf_counter()
         ws = vecchia.assemble(ordered, plan, spec, out=ws)
