@@ -40,7 +40,7 @@ int big_slot_map(int nt, SlotMap* map) {
       } else {
         slot_end[chosen] = e0;
       }
-      map->s[ws::tidx(I, k, nt)] = (int16_t)chosen;
+      map->s[ws::tidx(I, k, nt)] = chosen;
     }
   }
   cached_nt = nt;

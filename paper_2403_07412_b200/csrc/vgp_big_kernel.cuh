@@ -79,7 +79,7 @@ __host__ __device__ inline int head_doubles(int m, int kind = kMaternGen) {
 // instead of 3.  The global-scratch path keeps the plain triangle.
 constexpr int kMaxSlotTiles = 528;  // NT <= 32
 struct SlotMap {
-  int16_t s[kMaxSlotTiles];
+  int32_t s[kMaxSlotTiles];  // 32-bit: no byte permutes on the lookups
 };
 int big_slot_map(int nt, SlotMap* map);  // returns the slot count
 

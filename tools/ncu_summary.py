@@ -60,7 +60,7 @@ def main(rep, blocks=None, out_json=None):
     for k in hdr:
         if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
             try:
-                stall[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = int(raw[k].replace(",", ""))
+                stall[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = int(raw[k].split()[0].replace(",", ""))
             except ValueError:
                 pass
     st = sum(stall.values()) or 1
