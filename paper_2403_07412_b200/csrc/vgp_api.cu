@@ -785,7 +785,7 @@ static int plan_create(int device, int64_t n, int32_t m, int metric, double radi
     if (want && bytes < freeb / 2) {
       if (cudaMalloc((void**)&p->d_dcache, bytes) == cudaSuccess &&
           cudaMalloc((void**)&p->d_prev_locs, sizeof(double) * 2 * (size_t)n) == cudaSuccess &&
-          cudaMalloc((void**)&p->d_flag, sizeof(int)) == cudaSuccess) {
+          cudaMalloc((void**)&p->d_flag, 4 * sizeof(int)) == cudaSuccess) {  // flag | pad | max distance (u64)
         p->dcache_stride = stride;
       } else {
         cudaFree(p->d_dcache);
@@ -1003,6 +1003,11 @@ int vgp_plan_set_data(vgp_plan* plan, const double* locations, const double* obs
                                    cudaMemcpyDeviceToDevice, p->stream));
       VGP_CUDA_TRY(launch_build_dcache(*p, p->stream));
       p->dcache_valid = true;
+      unsigned long long* hmax = (unsigned long long*)(p->h_small + 7);
+      VGP_CUDA_TRY(cudaMemcpyAsync(hmax, p->d_flag + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   p->stream));
+      VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));
+      std::memcpy(&p->dcache_dmax, hmax, sizeof(double));
     }
   }
   VGP_CUDA_TRY(cudaStreamSynchronize(p->stream));

@@ -19,7 +19,9 @@ constexpr int kWarps = 4;
 __global__ void __launch_bounds__(kWarps * 32)
 build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m,
                     int64_t e_lo, int64_t e_hi, int64_t rest_lo, double* __restrict__ cache,
-                    int64_t cstride, int metric, double radius) {
+                    int64_t cstride, int metric, double radius,
+                    unsigned long long* __restrict__ dmax) {
+  double dm = 0.0;  // largest cached distance (the K_nu table's shared window)
   extern __shared__ double2 sxy[];  // kWarps x (m + 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* XY = sxy + warp * (m + 1);
@@ -55,9 +57,13 @@ build_dcache_kernel(const double4* __restrict__ pts, const int32_t* __restrict__
         }
       }
       out[t * 64 + ws::chunk_off(rr, col >> 1) + (col & 1)] = d;
+      dm = fmax(dm, d);
     }
     __syncwarp();
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, off));
+  if (lane == 0 && dmax) atomicMax(dmax, (unsigned long long)__double_as_longlong(dm));
 }
 
 __global__ void diff_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
@@ -77,8 +83,10 @@ cudaError_t launch_build_dcache(const Plan& p, cudaStream_t stream) {
   const int64_t want = (e_hi - e_lo + kWarps - 1) / kWarps;
   const int grid = (int)(want < (int64_t)p.num_sms * 8 ? want : (int64_t)p.num_sms * 8);
   const size_t sm = sizeof(double2) * kWarps * (p.m + 1);
-  build_dcache_kernel<<<grid, kWarps * 32, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi,
-                                                          p.rest_lo, p.d_dcache, p.dcache_stride, p.metric, p.radius);
+  if (p.d_flag) cudaMemsetAsync(p.d_flag + 2, 0, sizeof(unsigned long long), stream);
+  build_dcache_kernel<<<grid, kWarps * 32, sm, stream>>>(
+      p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, p.d_dcache, p.dcache_stride, p.metric, p.radius,
+      p.d_flag ? reinterpret_cast<unsigned long long*>(p.d_flag + 2) : nullptr);
   return cudaGetLastError();
 }
 

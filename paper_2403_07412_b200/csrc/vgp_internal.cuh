@@ -96,6 +96,7 @@ struct Plan {
   double* d_dcache = nullptr;   // per-block distance cache (ws:: tile layout)
   int64_t dcache_stride = 0;    // doubles per block (16-byte multiple)
   bool dcache_valid = false;
+  double dcache_dmax = 0.0;     // largest cached distance (K_nu table shared-memory window)
   double* d_prev_locs = nullptr;  // locations the cache was built from (n x 2)
   int* d_flag = nullptr;
   bool timing = false;          // record events around the fused kernel

@@ -22,6 +22,8 @@
 // like scipy's kv.
 #pragma once
 
+#include <cmath>
+
 #include "vgp_internal.cuh"
 #include "vgp_math.cuh"
 
@@ -41,9 +43,25 @@ static __device__ __noinline__ double matern_gen_exact(double u, const CovParams
 }
 
 // C(u) from the table; e_neg(u) must return s2 * e^-u (the caller's lean exp)
+// A kernel may stage a window of kKtabWinSeg consecutive segments (14
+// binades) in shared memory, starting at segment wseg0 (ktab_window); the
+// evaluation reads those with LDS, the rest from the global table.
+constexpr int kKtabWinSeg = 14 * kKtabSeg;
+
+inline int ktab_window(double dmax, double inv_beta) {
+  // the 14 binades below the largest u = d_max / beta of the plan's cache
+  if (!(dmax > 0.0)) return -(1 << 30);
+  int b = (int)std::floor(std::log2(dmax * inv_beta));
+  if (b > kKtabOMax) b = kKtabOMax;
+  int lo = b - 13;
+  if (lo < kKtabOMin) lo = kKtabOMin;
+  return (lo - kKtabOMin) * kKtabSeg;
+}
+
 template <typename ExpNeg>
 __device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ ktab,
-                                           const CovParams& cp, ExpNeg e_neg) {
+                                           const CovParams& cp, ExpNeg e_neg,
+                                           const double* ktw = nullptr, int wseg0 = 0) {
   const int hi = __double2hiint(u);
   const int lo = __double2loint(u);
   const int bex = hi >> 20;  // biased exponent (u >= 0)
@@ -58,8 +76,20 @@ __device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ 
   const int seg = ((hi >> 14) & 0x1FFFF) - ((1023 + kKtabOMin) << 6);
   const double d = __hiloint2double((hi & 0x3FFF) | 0x3FF00000, lo);
   const double t = fma(d, 128.0, -129.0);
-  const double2* c = reinterpret_cast<const double2*>(ktab + (size_t)seg * 8);
-  const double2 c01 = __ldg(c), c23 = __ldg(c + 1), c45 = __ldg(c + 2), c67 = __ldg(c + 3);
+  double2 c01, c23, c45, c67;
+  if (ktw && (unsigned)(seg - wseg0) < (unsigned)kKtabWinSeg) {
+    const double2* c = reinterpret_cast<const double2*>(ktw + (seg - wseg0) * 8);
+    c01 = c[0];
+    c23 = c[1];
+    c45 = c[2];
+    c67 = c[3];
+  } else {
+    const double2* c = reinterpret_cast<const double2*>(ktab + (size_t)seg * 8);
+    c01 = __ldg(c);
+    c23 = __ldg(c + 1);
+    c45 = __ldg(c + 2);
+    c67 = __ldg(c + 3);
+  }
   double p = fma(c67.y, t, c67.x);
   p = fma(p, t, c45.y);
   p = fma(p, t, c45.x);

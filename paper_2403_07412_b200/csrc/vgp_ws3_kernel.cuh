@@ -69,11 +69,16 @@ constexpr int kTraceEvents = ws::kTraceEvents;
 // the per-evaluation polynomial table (vgp_ktab.cuh) with the same lean exp
 template <int KIND>
 __device__ __forceinline__ double cov_gen(double d, double inv_beta, const double* tab,
-                                          const double* __restrict__ ktab, const CovParams& cp) {
+                                          const double* __restrict__ ktab, const CovParams& cp,
+                                          const double* ktw = nullptr, int wseg0 = 0) {
   if constexpr (KIND != kMaternGen) return cov_lean<KIND>(d, inv_beta, tab);
   return cov_ktab(d * inv_beta, ktab, cp,
-                  [&](double u) { return cov_lean<kMatern05>(u, 1.0, tab); });
+                  [&](double u) { return cov_lean<kMatern05>(u, 1.0, tab); }, ktw, wseg0);
 }
+// the K_nu table window in shared memory (general nu, NT = 8: the smem left
+// beside the eight slots holds 14 binades)
+template <int KIND, int NT>
+constexpr bool kTabWindow = KIND == kMaternGen && NT == 8;
 
 struct SlotLayout {
   int tiles;   // doubles of the tile triangle (= cache stride)
@@ -94,7 +99,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
                   const double* __restrict__ dcache, int64_t cstride,
-                  const double* __restrict__ ktab, const CovParams cpx,
+                  const double* __restrict__ ktab, const CovParams cpx, int wseg0,
                   long long* __restrict__ trace = nullptr) {
   constexpr int P = 8 * NT;
   const int m = MC > 0 ? MC : m_rt;
@@ -116,6 +121,15 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   // 2s = tile column staged (worker -> chain), 2s + 1 = L written (chain -> worker)
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) smem[i] = s2 * kExp2Table[i];
+  double* ktw = nullptr;
+  if constexpr (kTabWindow<KIND, NT>) {
+    if (wseg0 >= 0) {
+      ktw = smem + kHead + kSlots * L.stride;
+      const double2* src = reinterpret_cast<const double2*>(ktab + (size_t)wseg0 * 8);
+      const int nwin = min(kKtabWinSeg, kKtabSegments - wseg0) * 4;  // double2 per segment: 4
+      for (int i = threadIdx.x; i < nwin; i += blockDim.x) reinterpret_cast<double2*>(ktw)[i] = __ldg(src + i);
+    }
+  }
   if (CACHE && warp < kSlots && lane == 0) mbar_init(MBb(warp));
   if (CG && warp < kSlots && lane < 2) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(dmma::smem_u32(GBb(warp) + lane)));
@@ -249,8 +263,8 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
                 double v0, v1;
                 if (CACHE) {
                   const double2 dv = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
-                  v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx);
-                  v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx);
+                  v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx, ktw, wseg0);
+                  v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx, ktw, wseg0);
                 } else {
                   const double2* XY = XYb(s);
                   const double2 pa = XY[i];
@@ -339,8 +353,8 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
           const int i = 8 * I + r;
           double* tp = T + tidx(I, c, NT) * 64 + chunk_off(r, q);
           const double2 dv = ld2(tp);
-          double v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx);
-          double v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx);
+          double v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx, ktw, wseg0);
+          double v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx, ktw, wseg0);
           if (I == NT - 1 && i > m) {  // row m+1: yJ (0 from column m on); padding: 0
             const double2 ov = ld2(Ob(s) + 8 * c + 2 * q);
             v0 = i == m + 1 ? ov.x : 0.0;
@@ -495,7 +509,9 @@ template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = fa
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, long long* trace = nullptr) {
   constexpr SlotLayout L = slot_layout(NT);
-  const size_t sm = sizeof(double) * ((size_t)kHead + (size_t)kSlots * L.stride);
+  const int wseg0 = kTabWindow<KIND, NT> ? ktab_window(p.dcache_dmax, cp.inv_beta) : -(1 << 30);
+  const size_t sm = sizeof(double) * ((size_t)kHead + (size_t)kSlots * L.stride +
+                                      (kTabWindow<KIND, NT> ? (size_t)kKtabWinSeg * 8 : 0));
   static size_t configured[64] = {};
   const int dev = p.device & 63;
   auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE, CG>;
@@ -510,7 +526,8 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   const int grid = (int)(want < cap ? want : cap);
   kern<<<grid, kThreads, sm, stream>>>(p.d_pts, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp.s2,
                                        cp.inv_beta, p.d_rest, p.d_mu, p.d_sig, p.d_fail,
-                                       p.d_dcache, p.dcache_stride, p.d_ktab, cp, trace);
+                                       p.d_dcache, p.dcache_stride, p.d_ktab, cp,
+                                       wseg0 >= 0 ? wseg0 : -1, trace);
   return cudaGetLastError();
 }
 
