@@ -2,10 +2,14 @@
 
 Workload (BASELINE config 2): n = 1,000,000 uniform locations in [0,1]^2,
 m = 60, random ordering (seed 0), Matérn nu = 1.5, sigma^2 = 1,
-beta = 0.052537 (vg/kernels.py:118), FP64.  One "step" = one full
-log-likelihood evaluation (all n - m + 1 blocks, fused kernel + ordered
-reduction) of the same plan.  Inputs (32 MB points + 240 MB int32 neighbour
-table) exceed the 126 MB L2, so no explicit flush is needed between steps.
+beta = 0.052537 (vg/kernels.py:118), FP64; observations drawn by the device
+Vecchia forward simulation at those parameters.  One "step" =
+one full log-likelihood evaluation (all n - m + 1 blocks, fused kernel +
+ordered reduction) of the same plan.  Inputs (32 MB points + 240 MB int32
+neighbour table + the 18 GB distance cache) exceed the 126 MB L2, so no
+explicit flush is needed between steps.  The cpu_baseline leg doubles as
+the run's parity check (`parity`: the oracle over the same blocks, the
+oracle's neighbour table over the first 200k targets).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
