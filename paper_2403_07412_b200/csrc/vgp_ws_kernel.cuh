@@ -73,7 +73,7 @@ struct PairLayout {
   int stride;  // doubles per pair: tiles | S (2 tiles) | O (P) | XY (2P) | yt (4) | mbarrier (2)
 };
 __host__ __device__ constexpr PairLayout pair_layout(int nt) {
-  return PairLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 4 + 2};
+  return PairLayout{ntri(nt) * 64, ntri(nt) * 64 + 128 + 8 * nt + 16 * nt + 4 + 2 + 16};
 }
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
@@ -117,6 +117,7 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
   double2* XY = reinterpret_cast<double2*>(O + P);
   double* misc = O + 3 * P;  // [0] sigma_new, [1] -mu, [2 + parity] target obs
   uint64_t* mbar = reinterpret_cast<uint64_t*>(misc + 4);
+  double* Lcb = misc + 6;  // [pivot parity][8] column of L_cc (chain broadcast)
   const int cbar = 1 + 2 * pr;  // column c staged (worker -> chain)
   const int lbar = 2 + 2 * pr;  // L of column c written (chain -> worker)
 
@@ -330,12 +331,24 @@ loglik_ws_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nb
                   const double nxt = fma(-a[0][j], a[0][j], a[0][j + 1]);
                   piv = shfl(nxt, j + 1);
                 }
+                // column j of L_cc through shared memory (one store, four
+                // broadcast LDS.128 instead of 14 32-bit shuffles; double-
+                // buffered by pivot parity, one __syncwarp per pivot)
+                double* Lc = Lcb + 8 * (j & 1);
+                if (lane < 8) Lc[lane] = a[0][j];
+                __syncwarp();
+                double lcv[8];
+#pragma unroll
+                for (int x = (j + 1) & ~1; x < 8; x += 2) {
+                  const double2 v = ld2(Lc + x);
+                  lcv[x] = v.x;
+                  lcv[x + 1] = v.y;
+                }
 #pragma unroll
                 for (int jp = j + 1; jp < 8; ++jp) {
-                  const double lc = shfl(a[0][j], jp);  // L[R0 + jp][R0 + j]
 #pragma unroll
                   for (int rr = 0; rr < kMaxRows; ++rr)
-                    if (rr * 32 < NR) a[rr][jp] = fma(-a[rr][j], lc, a[rr][jp]);
+                    if (rr * 32 < NR) a[rr][jp] = fma(-a[rr][j], lcv[jp], a[rr][jp]);
                 }
               }
             }
