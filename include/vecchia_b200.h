@@ -203,6 +203,16 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
 int vgp_simulate(vgp_plan* plan, int family, double sigma_sq, double beta, double nu,
                  const double* z, double* y, int64_t* fail_index);
 
+/* vgp_plan_set_data + vgp_loglik in one call (what vecchia_loglik does per
+ * evaluation).  When the plan already holds a distance cache, the
+ * observations are uploaded and the evaluation starts while the locations
+ * upload on another stream and are compared with the cache's; if they
+ * differ the cache is rebuilt and the evaluation rerun before returning —
+ * the result is always that of the new dataset.  Synchronous. */
+int vgp_loglik_data(vgp_plan* plan, const double* locations, const double* observations, int family,
+                    double sigma_sq, double beta, double nu, double* total, int64_t* fail_index,
+                    double* block_first, double* block_rest, double* mu_new, double* sigma_new);
+
 /* Shard form for multi-GPU evaluation: the plan's fixed 4096-chunk partial
  * sums of block_rest (partials: plan's chunk count, see vgp_plan_info) and,
  * when the plan holds entry 0, block_first (else 0).  Summing every shard's

@@ -45,7 +45,7 @@ EXPORTS = (
     "vgp_batch_potrf", "vgp_batch_trsv", "vgp_batch_dot", "vgp_loglik_partials_device",
     "vgp_plan_set_timing", "vgp_plan_kernel_time", "vgp_maxmin_order", "vgp_assemble",
     "vgp_simulate", "vgp_knn_predecessors_range",
-    "vgp_plan_create_shard", "vgp_plan_fail_keys",
+    "vgp_plan_create_shard", "vgp_plan_fail_keys", "vgp_loglik_data",
 )
 
 
@@ -105,6 +105,7 @@ _sig("vgp_knn_predecessors_range", _int, [_int, _dp, _i64, _i32, _i64, _i64, _ip
 _sig("vgp_plan_create_shard", _int, [_int, _i64, _i32, _int, _d, _ip, _ip, _i64, _i64,
                                     ctypes.POINTER(_vp)])
 _sig("vgp_plan_fail_keys", _int, [_vp, ctypes.POINTER(ctypes.c_uint64)])
+_sig("vgp_loglik_data", _int, [_vp, _dp, _dp, _int, _d, _d, _d, _dp, _ip, _dp, _dp, _dp, _dp])
 _sig("vgp_simulate", _int, [_vp, _int, _d, _d, _d, _dp, _dp, _ip])
 _sig("vgp_loglik_partials", _int, [_vp, _int, _d, _d, _d, _dp, _dp, _ip])
 _sig("vgp_plan_info", _int, [_vp, _ip])

@@ -167,6 +167,7 @@ void free_plan(Plan* p) {
   }
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->side) cudaStreamDestroy(p->side);
+  if (p->aux) cudaStreamDestroy(p->aux);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   for (auto ev : p->ev_chunk)
@@ -739,6 +740,7 @@ static int plan_create(int device, int64_t n, int32_t m, int metric, double radi
   const int64_t nrest = p->rest_hi - p->rest_lo;
   cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
   for (int i = 0; i < 8 && e == cudaSuccess; ++i)
@@ -1150,6 +1152,50 @@ int vgp_loglik(vgp_plan* plan, int family, double sigma_sq, double beta, double 
   if (total) *total = st == VGP_OK ? sc[0] : NAN;
   if (block_first) *block_first = st == VGP_OK ? sc[1] : NAN;
   return st;
+}
+
+int vgp_loglik_data(vgp_plan* plan, const double* locations, const double* observations, int family,
+                    double sigma_sq, double beta, double nu, double* total, int64_t* fail_index,
+                    double* block_first, double* block_rest, double* mu_new, double* sigma_new) {
+  if (!plan || !locations || !observations) return fail(VGP_E_INVALID, "null pointer");
+  Plan* p = &plan->p;
+  if (!(p->blk_lo == 0 && p->blk_hi == p->n - p->m + 1))
+    return fail(VGP_E_INVALID, "vgp_loglik_data needs a plan over all blocks");
+  CovParams cp;
+  int rc = make_cov_params(family, sigma_sq, beta, nu, &cp);
+  if (rc) return rc;
+  const bool spec = p->has_data && p->d_dcache && p->dcache_valid && p->aux;
+  if (!spec) {
+    rc = vgp_plan_set_data(plan, locations, observations);
+    if (rc) return rc;
+    return vgp_loglik(plan, family, sigma_sq, beta, nu, total, fail_index, block_first, block_rest,
+                      mu_new, sigma_new);
+  }
+  DeviceGuard g(p->device);
+  const int64_t n = p->n;
+  // Speculate that the locations are the ones the distance cache was built
+  // from (an MLE loop re-evaluates one dataset): the observations go up and
+  // the evaluation starts; the locations go up on another stream and are
+  // compared with the cache's next to it.  If they differ, the cache is
+  // rebuilt and the evaluation rerun before returning.
+  VGP_CUDA_TRY(cudaMemcpyAsync(p->d_raw + 2 * n, observations, sizeof(double) * n,
+                               cudaMemcpyHostToDevice, p->stream));
+  VGP_CUDA_TRY(launch_permute_obs(p->d_raw + 2 * n, p->d_order, n, p->d_pts, p->stream));
+  int* hflag = (int*)(p->h_small + 6);
+  VGP_CUDA_TRY(cudaMemcpyAsync(p->d_raw, locations, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, p->aux));
+  VGP_CUDA_TRY(cudaMemsetAsync(p->d_flag, 0, sizeof(int), p->aux));
+  VGP_CUDA_TRY(launch_diff(p->d_raw, p->d_prev_locs, 2 * n, p->d_flag, p->aux));
+  VGP_CUDA_TRY(cudaMemcpyAsync(hflag, p->d_flag, sizeof(int), cudaMemcpyDeviceToHost, p->aux));
+  rc = vgp_loglik(plan, family, sigma_sq, beta, nu, total, fail_index, block_first, block_rest, mu_new,
+                  sigma_new);
+  VGP_CUDA_TRY(cudaStreamSynchronize(p->aux));
+  if (*hflag == 0) return rc;
+  // the locations changed: the full upload path (permute, rebuild the
+  // cache and its d_max), then evaluate again
+  rc = vgp_plan_set_data(plan, locations, observations);
+  if (rc) return rc;
+  return vgp_loglik(plan, family, sigma_sq, beta, nu, total, fail_index, block_first, block_rest, mu_new,
+                    sigma_new);
 }
 
 int vgp_plan_fail_keys(vgp_plan* plan, uint64_t* keys) {

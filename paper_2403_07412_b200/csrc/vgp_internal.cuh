@@ -66,6 +66,7 @@ struct Plan {
   int64_t rest_lo = 0, rest_hi = 0;  // block_rest indices k = e - 1 covered by this plan
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // joint block and result downloads overlap the main kernel
+  cudaStream_t aux = nullptr;   // vgp_loglik_data: location upload + check next to the evaluation
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_chunk[8] = {};
   int64_t* d_order = nullptr;   // n, ordered position -> original index
@@ -151,6 +152,10 @@ cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t 
 // non-positive-definite entry (initialise to ~0).
 cudaError_t launch_simulate(const Plan& p, const CovParams& cp, const double* d_z, double* d_y,
                             unsigned long long* d_fail, cudaStream_t stream);
+
+// Permute only the observations into pts[i].z (locations unchanged).
+cudaError_t launch_permute_obs(const double* d_obs, const int64_t* d_order, int64_t n, double4* d_pts,
+                               cudaStream_t stream);
 
 // Generic per-block likelihood kernel (any m; smem- or global-resident block).
 cudaError_t launch_loglik_generic(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,

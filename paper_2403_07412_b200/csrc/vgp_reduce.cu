@@ -20,6 +20,14 @@ __global__ void permute_kernel(const double* __restrict__ raw, const int64_t* __
   pts[i] = make_double4(xy.x, xy.y, raw[2 * n + s], 0.0);
 }
 
+// observations only (the locations are unchanged): pts[i].z
+__global__ void permute_obs_kernel(const double* __restrict__ obs, const int64_t* __restrict__ order,
+                                   int64_t n, double4* __restrict__ pts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  reinterpret_cast<double*>(pts)[4 * i + 2] = obs[order[i]];
+}
+
 // One warp per 4096-chunk.  A full chunk is a perfect binary tree of 32
 // numpy 128-blocks: lane l sums block l with numpy's 8-accumulator rule and
 // the xor-shuffle tree reproduces numpy's split-in-half recursion exactly.
@@ -104,6 +112,12 @@ cudaError_t launch_permute(const double* d_raw, const int64_t* d_order, int64_t 
                            cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   permute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_raw, d_order, n, d_pts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_obs(const double* d_obs, const int64_t* d_order, int64_t n, double4* d_pts,
+                               cudaStream_t stream) {
+  permute_obs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_obs, d_order, n, d_pts);
   return cudaGetLastError();
 }
 

@@ -207,8 +207,7 @@ class DevicePlan:
         CTA-per-block, 13 thread-per-block."""
         N.check(N.lib.vgp_plan_set_variant(self.handle, int(variant)))
 
-    def set_data(self, dataset: geo.Dataset) -> None:
-        """Upload a dataset in original order; the device applies the permutation."""
+    def _host_arrays(self, dataset: geo.Dataset):
         if dataset.n != self.n:
             raise ValueError(f"plan built for n={self.n}, dataset has n={dataset.n}")
         locs = np.ascontiguousarray(dataset.locations, dtype=np.float64)
@@ -216,15 +215,25 @@ class DevicePlan:
         if locs is dataset.locations and obs is dataset.observations:
             _pin(locs)
             _pin(obs)
+        return locs, obs
+
+    def set_data(self, dataset: geo.Dataset) -> None:
+        """Upload a dataset in original order; the device applies the permutation."""
+        locs, obs = self._host_arrays(dataset)
         N.check(N.lib.vgp_plan_set_data(self.handle, N.dptr(locs), N.dptr(obs)))
 
     @property
     def stream(self) -> int:
         return int(N.lib.vgp_plan_stream(self.handle) or 0)
 
-    def loglik(self, spec: kernels.KernelSpec, full_result: bool = True) -> LogLikResult:
+    def loglik(self, spec: kernels.KernelSpec, full_result: bool = True,
+               dataset: geo.Dataset | None = None) -> LogLikResult:
+        """Evaluate at `spec`; with `dataset`, upload it first in the same
+        call (vgp_loglik_data: the location upload and check overlap the
+        evaluation when the plan's distance cache already holds them)."""
         if not self.full:
             raise ValueError("loglik needs a full-range plan; use partials() on shards")
+        host = self._host_arrays(dataset) if dataset is not None else None
         p = spec.params
         k = self.n - self.m
         total = np.zeros(1)
@@ -236,9 +245,12 @@ class DevicePlan:
         else:
             rest = mu = sg = None
             ptrs = (N.null_d(), N.null_d(), N.null_d())
-        rc = N.lib.vgp_loglik(self.handle, N.FAMILY_CODES[spec.family], float(p.sigma_sq),
-                              float(p.beta), float(p.nu), N.dptr(total), N.iptr(fail),
-                              N.dptr(bf), *ptrs)
+        args = (N.FAMILY_CODES[spec.family], float(p.sigma_sq), float(p.beta), float(p.nu),
+                N.dptr(total), N.iptr(fail), N.dptr(bf), *ptrs)
+        if host is not None:
+            rc = N.lib.vgp_loglik_data(self.handle, N.dptr(host[0]), N.dptr(host[1]), *args)
+        else:
+            rc = N.lib.vgp_loglik(self.handle, *args)
         N.raise_for_status(rc, int(fail[0]))
         if not full_result:
             rest = mu = sg = np.empty(0)
@@ -411,8 +423,7 @@ def vecchia_loglik(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.Kernel
     if plan.permutation.n != dataset.n:
         raise ValueError(f"plan built for n={plan.permutation.n}, dataset has n={dataset.n}")
     dp = plan.device_plan(metric=dataset.metric)
-    dp.set_data(dataset)
-    return dp.loglik(spec)
+    return dp.loglik(spec, dataset=dataset)
 
 
 def simulate_vecchia(dataset: geo.Dataset, plan: VecchiaPlan, spec: kernels.KernelSpec,

@@ -354,6 +354,16 @@ def test_distance_cache_rebuilt_when_locations_change(vg, oracle):
     ref = oracle.loglik(ordered.locations, ordered.observations, int(z["m"]), z["table"], "matern",
                         *[float(v) for v in z["theta"]])
     assert rel(got, ref.total) <= TOL_TOTAL
+    # back to the original locations (speculation misses, cache rebuilt),
+    # then new observations only (speculation hits): each equals the
+    # separate upload + evaluation bit for bit
+    dp = plan.device_plan()
+    for ds in (data, vg.Dataset(z["locs"], z["obs"][::-1].copy())):
+        fused = vg.vecchia_loglik(ds, plan, spec)
+        dp.set_data(ds)
+        sep = dp.loglik(spec)
+        assert fused.total == sep.total
+        np.testing.assert_array_equal(fused.block_rest, sep.block_rest)
 
 
 @pytest.mark.parametrize("m,variant", [(30, -1), (90, -1)])
