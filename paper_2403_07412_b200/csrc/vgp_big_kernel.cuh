@@ -35,6 +35,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "vgp_ktab.cuh"
 #include "vgp_math.cuh"
 #include "vgp_ws_kernel.cuh"
@@ -202,12 +204,17 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
     // stage them (natural column order)
     auto column_work = [&](const int J, const int kmax, const int w0, const int nw) {
         for (int I0 = J + (warp - w0); I0 < NT; I0 += nw * kGroup) {
-          double acc[kGroup][2];
+          // active tiles of this group (warp-uniform), dispatched to a body
+          // unrolled for exactly that many: a predicated-off DMMA still
+          // occupies the FP64 datapath (ncu: 2464 DMMA issued per m = 120
+          // block against 1360 needed when the tail groups were predicated)
+          const int ng = min(kGroup, (NT - 1 - I0) / nw + 1);
+          auto group = [&](auto ngc) {
+            constexpr int NG = decltype(ngc)::value;
+            double acc[NG][2];
 #pragma unroll
-          for (int g = 0; g < kGroup; ++g) {
-            const int I = I0 + g * nw;
-            acc[g][0] = acc[g][1] = 0.0;
-            if (I < NT) {
+            for (int g = 0; g < NG; ++g) {
+              const int I = I0 + g * nw;
               const int i = 8 * I + r;
               double v0, v1;
               const int j0 = 8 * J + 2 * q;  // columns j0, j0 + 1
@@ -232,26 +239,27 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
               acc[g][0] = v0;
               acc[g][1] = v1;
             }
-          }
-          // active tiles of this group (warp-uniform): inactive slots issue no
-          // loads and no DMMAs
-          const int ng = min(kGroup, (NT - 1 - I0) / nw + 1);
-          for (int k = 0; k <= kmax; ++k) {
-            const double2 b = ld2(tile(J, k) + chunk_off(r, q));
-            double2 a[kGroup];
+            for (int k = 0; k <= kmax; ++k) {
+              const double2 b = ld2(tile(J, k) + chunk_off(r, q));
+              double2 a[NG];
 #pragma unroll
-            for (int g = 0; g < kGroup; ++g)
-              if (g < ng) a[g] = ld2(tile(I0 + g * nw, k) + chunk_off(r, q));
+              for (int g = 0; g < NG; ++g) a[g] = ld2(tile(I0 + g * nw, k) + chunk_off(r, q));
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
+              for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
-              for (int g = 0; g < kGroup; ++g)
-                if (g < ng) mma(acc[g][0], acc[g][1], neg(kk ? a[g].y : a[g].x), kk ? b.y : b.x);
+                for (int g = 0; g < NG; ++g) mma(acc[g][0], acc[g][1], neg(kk ? a[g].y : a[g].x), kk ? b.y : b.x);
+              }
             }
-          }
 #pragma unroll
-          for (int g = 0; g < kGroup; ++g)
-            if (I0 + g * nw < NT) st2(tile(I0 + g * nw, J) + chunk_off(r, q), acc[g][0], acc[g][1]);
+            for (int g = 0; g < NG; ++g) st2(tile(I0 + g * nw, J) + chunk_off(r, q), acc[g][0], acc[g][1]);
+          };
+          static_assert(kGroup == 4, "group dispatch below");
+          switch (ng) {
+            case 4: group(std::integral_constant<int, 4>{}); break;
+            case 3: group(std::integral_constant<int, 3>{}); break;
+            case 2: group(std::integral_constant<int, 2>{}); break;
+            default: group(std::integral_constant<int, 1>{}); break;
+          }
         }
     };
     // the last left-looking step of tile column J: reload, apply L of column
