@@ -1,5 +1,6 @@
 // Large-m CTA-per-block DMMA kernel (vgp_big_kernel.cuh): host helpers and the
 // family dispatch (instantiations in vgp_big_k*.cu, compiled in parallel).
+#include <mutex>
 #include <vector>
 
 #include "vgp_big_kernel.cuh"
@@ -16,6 +17,8 @@ namespace big {
 int big_slot_map(int nt, SlotMap* map) {
   // lifetimes in tile-column steps: tile (I, k) is written by the look-ahead
   // at step k - 1 and last read at step I - 1 (the diagonal tile at step k)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   static int cached_nt = -1, cached_slots = 0;
   static SlotMap cached;
   if (nt == cached_nt) {
@@ -40,7 +43,7 @@ int big_slot_map(int nt, SlotMap* map) {
       } else {
         slot_end[chosen] = e0;
       }
-      map->s[ws::tidx(I, k, nt)] = chosen;
+      map->s[I * kSlotStride + k] = chosen * 64 * (int)sizeof(double);
     }
   }
   cached_nt = nt;

@@ -80,8 +80,12 @@ __host__ __device__ inline int head_doubles(int m, int kind = kMaternGen) {
 // big_slot_map).  m = 120: 73 slots instead of 136 tiles, 4 CTAs per SM
 // instead of 3.  The global-scratch path keeps the plain triangle.
 constexpr int kMaxSlotTiles = 528;  // NT <= 32
+constexpr int kSlotStride = 32;
 struct SlotMap {
-  int32_t s[kMaxSlotTiles];  // 32-bit: no byte permutes on the lookups
+  // byte offset of tile (I, J) at [I * kSlotStride + J]: row-major, so the
+  // left-looking k loop walks consecutive entries (no triangular index
+  // arithmetic); 32-bit, no byte permutes on the lookups
+  int32_t s[kSlotStride * kSlotStride];
 };
 int big_slot_map(int nt, SlotMap* map);  // returns the slot count
 
@@ -164,7 +168,8 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
   __syncthreads();
   const double* tab = smem;
   auto tile = [&](int I, int J) -> double* {
-    return T + (size_t)(SLOTS ? smap.s[tidx(I, J, NT)] : tidx(I, J, NT)) * 64;
+    if (SLOTS) return reinterpret_cast<double*>(reinterpret_cast<char*>(T) + smap.s[I * kSlotStride + J]);
+    return T + (size_t)tidx(I, J, NT) * 64;
   };
   // block eb's point rows: lane l of warp 1 gathers rows 4l..4l+3 (P / 4 <= 32
   // lanes per pass): neighbours a < m, the target at a = m, row 0 as padding
@@ -236,8 +241,11 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
                 v0 = (i == m + 1 && j0 < m) ? G[j0].z : 0.0;
                 v1 = (i == m + 1 && j0 + 1 < m) ? G[j0 + 1].z : 0.0;
               }
-              acc[g][0] = v0;
-              acc[g][1] = v1;
+              // accumulate -A + sum L L^T and negate once at the store:
+              // bit-identical to A - sum L L^T (round-to-nearest is odd under
+              // negation) without negating an operand per DMMA
+              acc[g][0] = -v0;
+              acc[g][1] = -v1;
             }
             for (int k = 0; k <= kmax; ++k) {
               const double2 b = ld2(tile(J, k) + chunk_off(r, q));
@@ -247,11 +255,11 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
 #pragma unroll
               for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
-                for (int g = 0; g < NG; ++g) mma(acc[g][0], acc[g][1], neg(kk ? a[g].y : a[g].x), kk ? b.y : b.x);
+                for (int g = 0; g < NG; ++g) mma(acc[g][0], acc[g][1], kk ? a[g].y : a[g].x, kk ? b.y : b.x);
               }
             }
 #pragma unroll
-            for (int g = 0; g < NG; ++g) st2(tile(I0 + g * nw, J) + chunk_off(r, q), acc[g][0], acc[g][1]);
+            for (int g = 0; g < NG; ++g) st2(tile(I0 + g * nw, J) + chunk_off(r, q), -acc[g][0], -acc[g][1]);
           };
           static_assert(kGroup == 4, "group dispatch below");
           switch (ng) {
