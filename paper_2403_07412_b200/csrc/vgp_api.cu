@@ -385,7 +385,7 @@ int vgp_knn_predecessors_range(int device, const double* locations, int64_t n, i
     rc = dalloc(&d_pts, n);
     cudaError_t e = cudaSuccess;
     if (!rc) e = cudaMemcpyAsync(d_pts, locations, sizeof(double2) * n, cudaMemcpyHostToDevice, s);
-    if (!rc && e == cudaSuccess) e = knn_pred_grid(d_pts, locations, n, m, 32768, neighbors, s, row_lo, row_hi);
+    if (!rc && e == cudaSuccess) e = knn_pred_grid(d_pts, locations, n, m, int64_t(1) << 21, neighbors, s, row_lo, row_hi);
     if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (!rc && e != cudaSuccess) rc = fail(VGP_E_CUDA, std::string("knn (grid): ") + cudaGetErrorString(e));
     cudaFree(d_pts);

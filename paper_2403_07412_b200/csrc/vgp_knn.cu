@@ -116,10 +116,10 @@ knn_kernel(const PT* __restrict__ data, int64_t nd, const PT* __restrict__ query
 }
 
 // ---------------------------------------------------------------- grid search
-// Exact predecessor kNN in index batches (targets [s, e)): phase 1 searches
-// a uniform grid over the points [0, s) ring by ring, keeping the m smallest
-// (key, index) pairs; phase 2 is knn_kernel over the in-batch candidates
-// [s, i).  Phase 1 stops only when the current m-th key is strictly below a
+// Exact predecessor kNN in index batches (targets [s, e)): each target t
+// searches a uniform grid over the points [0, e) ring by ring, keeping the m
+// smallest (key, index) pairs among the candidates j < t.  The search stops
+// only when the current m-th key is strictly below a
 // lower bound of every key outside the searched square: the bound is the
 // target's distance to the square's boundary minus a slack that dominates
 // the cell-assignment rounding, squared with the key's own rounding (which
@@ -158,15 +158,28 @@ __device__ __forceinline__ bool lex_less(double k, int32_t j, double kq, int32_t
   return k < kq || (k == kq && j < jq);
 }
 
-// query q <-> ordered target t = t0 + q; scratch [slot * stride + q]
+// the grid's points in cell order (coordinates next to their index), so a
+// cell's candidates are one contiguous run
+__global__ void grid_gather_kernel(const double2* __restrict__ pts, const int32_t* __restrict__ ids_sorted,
+                                   int64_t s, double2* __restrict__ spts) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= s) return;
+  spts[p] = pts[ids_sorted[p]];
+}
+
+// query q <-> ordered target t = t0 + q, candidates j < t only (the grid may
+// hold later points of the batch); scratch [slot * stride + q]; the final
+// table row goes to out[q * m ..]
 __global__ void __launch_bounds__(kKnnThreads)
 grid_query_kernel(const double2* __restrict__ pts, int64_t t0, int64_t nq, int m, GridDesc gd,
                   const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
-                  const int32_t* __restrict__ cpts, double* __restrict__ keys, int32_t* __restrict__ idx,
-                  int64_t stride, int* __restrict__ cnt_out) {
+                  const int32_t* __restrict__ cpts, const double2* __restrict__ spts,
+                  double* __restrict__ keys, int32_t* __restrict__ idx, int64_t stride,
+                  int64_t* __restrict__ out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
-  const double2 pt = pts[t0 + q];
+  const int32_t t = (int32_t)(t0 + q);
+  const double2 pt = pts[t];
   const int g = gd.g;
   const int cx = cell_of(pt.x, gd.x0, gd.ihx, g), cy = cell_of(pt.y, gd.y0, gd.ihy, g);
   double* kp = keys + q;
@@ -208,7 +221,8 @@ grid_query_kernel(const double2* __restrict__ pts, int64_t t0, int64_t nq, int m
         const int b = cstart[c], e = cend[c];
         for (int pp = b; pp < e; ++pp) {
           const int32_t j = cpts[pp];
-          const double k = knn_key(pts[j], pt);
+          if (j >= t) continue;  // predecessors only (vg/geo.py:342)
+          const double k = knn_key(spts[pp], pt);
           if (cnt == m && !lex_less(k, j, wk, wj)) continue;
           int p;
           if (cnt == m) {
@@ -235,7 +249,8 @@ grid_query_kernel(const double2* __restrict__ pts, int64_t t0, int64_t nq, int m
       }
     }
   }
-  cnt_out[q] = cnt;
+  int64_t* o = out + q * (int64_t)m;
+  for (int x = 0; x < m; ++x) o[x] = (int64_t)ip[(int64_t)x * stride];
 }
 
 }  // namespace
@@ -264,9 +279,14 @@ cudaError_t launch_knn_sphere(const double4* d_data, int64_t nd, const double4* 
 
 namespace vgp {
 
-// Predecessor kNN (Euclidean) by index batches with a grid over the earlier
-// points; bit-identical to launch_knn's brute force (see grid_query_kernel).
-// locations are the ORDERED points (host); out (n - m) x m on the host.
+// Predecessor kNN (Euclidean) by index batches [s, e) with a grid over the
+// points [0, e): each target t searches it for candidates j < t only, so no
+// brute-force pass over the batch's own earlier points is needed (round 1 ran
+// one, 24x the grid search's time, profiles/r02_ncu_knn_grid.json).  Batches
+// grow geometrically (e <= 2 s): at least half of every grid is admissible to
+// each of its targets, and the last batches hold ~n/2 targets in one launch.
+// Bit-identical to launch_knn's brute force (see grid_query_kernel).
+// locations are the ORDERED points (host); out rows [row_lo, row_hi) on the host.
 cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n, int32_t m, int64_t batch,
                           int64_t* h_out, cudaStream_t st, int64_t row_lo, int64_t row_hi) {
   // rows [row_lo, row_hi) of the table (targets m + row); only points
@@ -280,12 +300,19 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
     y0 = std::min(y0, h_locs[2 * i + 1]);
     y1 = std::max(y1, h_locs[2 * i + 1]);
   }
-  const int64_t nqmax = std::max<int64_t>(1, std::min<int64_t>(batch, row_hi - row_lo));
+  // batch boundaries: e = min(n, s + batch cap, max(s + kMinBatch, 2 s))
+  constexpr int64_t kMinBatch = 4096;
+  auto batch_end = [&](int64_t s0) {
+    return std::min({n, s0 + batch, std::max(s0 + kMinBatch, 2 * s0)});
+  };
+  int64_t nqmax = 1;
+  for (int64_t s0 = m + row_lo; s0 < n; s0 = batch_end(s0)) nqmax = std::max(nqmax, batch_end(s0) - s0);
   const int64_t slots = ((nqmax + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
   const int gmax = 4096;
   uint32_t *cell = nullptr, *cell_s = nullptr;
-  int32_t *ids = nullptr, *ids_s = nullptr, *cs = nullptr, *ce = nullptr, *kidx = nullptr, *cnt = nullptr;
+  int32_t *ids = nullptr, *ids_s = nullptr, *cs = nullptr, *ce = nullptr, *kidx = nullptr;
   double* kkey = nullptr;
+  double2* spts = nullptr;
   int64_t* out = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
@@ -297,17 +324,17 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
   A((void**)&cell_s, sizeof(uint32_t) * n);
   A((void**)&ids, sizeof(int32_t) * n);
   A((void**)&ids_s, sizeof(int32_t) * n);
+  A((void**)&spts, sizeof(double2) * n);
   A((void**)&cs, sizeof(int32_t) * gmax * gmax);
   A((void**)&ce, sizeof(int32_t) * gmax * gmax);
   A((void**)&kkey, sizeof(double) * slots * m);
   A((void**)&kidx, sizeof(int32_t) * slots * m);
-  A((void**)&cnt, sizeof(int) * slots);
   A((void**)&out, sizeof(int64_t) * nqmax * m);
   A(&tmp, tmp_bytes);
-  for (int64_t s0 = m + row_lo; e == cudaSuccess && s0 < n; s0 += batch) {
-    const int64_t e0 = std::min(n, s0 + batch), nq = e0 - s0;
-    // grid over [0, s0): about 3 points per cell
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t)std::sqrt((double)s0 / 3.0)));
+  for (int64_t s0 = m + row_lo; e == cudaSuccess && s0 < n; s0 = batch_end(s0)) {
+    const int64_t e0 = batch_end(s0), nq = e0 - s0;
+    // grid over [0, e0): about 3 points per cell
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t)std::sqrt((double)e0 / 3.0)));
     GridDesc gd;
     gd.g = g;
     gd.x0 = x0;
@@ -320,26 +347,23 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
     gd.slack = 1e-9 * std::max(gd.hx, gd.hy) + 1e-12 * std::max({std::fabs(x0), std::fabs(x1), std::fabs(y0),
                                                                   std::fabs(y1)});
     const int bs = 256;
-    const unsigned nb = (unsigned)((s0 + bs - 1) / bs);
-    grid_cell_kernel<<<nb, bs, 0, st>>>(d_pts, s0, gd, cell, ids);
+    const unsigned nb = (unsigned)((e0 + bs - 1) / bs);
+    grid_cell_kernel<<<nb, bs, 0, st>>>(d_pts, e0, gd, cell, ids);
     e = cudaGetLastError();
     if (e == cudaSuccess)
-      e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_s, ids, ids_s, (int)s0, 0, 32, st);
+      e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, cell, cell_s, ids, ids_s, (int)e0, 0, 32, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(cs, 0, sizeof(int32_t) * g * g, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ce, 0, sizeof(int32_t) * g * g, st);
     if (e == cudaSuccess) {
-      grid_bounds_kernel<<<nb, bs, 0, st>>>(cell_s, s0, cs, ce);
+      grid_bounds_kernel<<<nb, bs, 0, st>>>(cell_s, e0, cs, ce);
+      grid_gather_kernel<<<nb, bs, 0, st>>>(d_pts, ids_s, e0, spts);
       e = cudaGetLastError();
     }
     const int64_t stride = ((nq + kKnnThreads - 1) / kKnnThreads) * kKnnThreads;
     const unsigned qb = (unsigned)(stride / kKnnThreads);
     if (e == cudaSuccess) {
-      grid_query_kernel<<<qb, kKnnThreads, 0, st>>>(d_pts, s0, nq, m, gd, cs, ce, ids_s, kkey, kidx, stride, cnt);
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) {
-      knn_kernel<double2><<<qb, kKnnThreads, 0, st>>>(d_pts, n, d_pts + s0, nq, s0 - m, 1, m, out, kkey, kidx,
-                                                      s0, cnt);
+      grid_query_kernel<<<qb, kKnnThreads, 0, st>>>(d_pts, s0, nq, m, gd, cs, ce, ids_s, spts, kkey, kidx,
+                                                    stride, out);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess)
@@ -350,11 +374,11 @@ cudaError_t knn_pred_grid(const double2* d_pts, const double* h_locs, int64_t n,
   cudaFreeAsync(cell_s, st);
   cudaFreeAsync(ids, st);
   cudaFreeAsync(ids_s, st);
+  cudaFreeAsync(spts, st);
   cudaFreeAsync(cs, st);
   cudaFreeAsync(ce, st);
   cudaFreeAsync(kkey, st);
   cudaFreeAsync(kidx, st);
-  cudaFreeAsync(cnt, st);
   cudaFreeAsync(out, st);
   cudaFreeAsync(tmp, st);
   return e;
