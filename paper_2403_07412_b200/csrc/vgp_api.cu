@@ -757,7 +757,8 @@ static int plan_create(int device, int64_t n, int32_t m, int metric, double radi
   if (!rc) rc = dalloc(&p->d_mu, nrest);
   if (!rc) rc = dalloc(&p->d_sig, nrest);
   if (!rc) rc = dalloc(&p->d_partials, std::max<int64_t>(p->chunk_hi - p->chunk_lo, 1));
-  if (!rc) rc = dalloc(&p->d_scalars, 4);
+  if (!rc) rc = dalloc(&p->d_scalars, 4);  // total | block_first | - | reduction ticket
+  if (!rc && cudaMemset(p->d_scalars, 0, 4 * sizeof(double)) != cudaSuccess) rc = fail(VGP_E_CUDA, "memset");
   if (!rc) rc = dalloc(&p->d_fail, 2);
   if (!rc) {
     // generic-path global workspace when a block does not fit in shared memory

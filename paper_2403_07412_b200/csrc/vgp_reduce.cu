@@ -28,48 +28,71 @@ __global__ void permute_obs_kernel(const double* __restrict__ obs, const int64_t
   reinterpret_cast<double*>(pts)[4 * i + 2] = obs[order[i]];
 }
 
-// One warp per 4096-chunk.  A full chunk is a perfect binary tree of 32
-// numpy 128-blocks: lane l sums block l with numpy's 8-accumulator rule and
-// the xor-shuffle tree reproduces numpy's split-in-half recursion exactly.
-// A short tail chunk is summed by lane 0 with the general recursion.
-__global__ void chunk_partials_kernel(const double* __restrict__ rest, int64_t rest_lo,
-                                      int64_t rest_hi, int64_t chunk_lo, int64_t chunk_hi,
-                                      double* __restrict__ partials) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = chunk_lo + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (c >= chunk_hi) return;
+// One 256-thread CTA per 4096-chunk.  A full chunk is a perfect binary tree
+// of 32 numpy 128-blocks (vg/vecchia.py:169-177 via numpy's pairwise sum):
+// thread (leaf l, accumulator j) runs numpy's j-th of 8 accumulators over
+// block l (the same 16 additions in the same order, 8x the parallelism of a
+// lane per block), a 3-level xor shuffle combines the 8 as numpy does
+// ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)), and the leaf tree is
+// numpy's split-in-half recursion: xor shuffles inside a warp (4 leaves),
+// shared memory across the 8 warps.  A short tail chunk is summed by one
+// thread with the general recursion.  With want_total, the last CTA to
+// finish adds the partials in chunk order, total = block_first +
+// ((0 + p0) + p1) + ... (vg/vecchia.py:213, :174-177), and rearms the ticket.
+__global__ void __launch_bounds__(256)
+chunk_partials_kernel(const double* __restrict__ rest, int64_t rest_lo, int64_t rest_hi,
+                      int64_t chunk_lo, int64_t chunk_hi, double* __restrict__ partials,
+                      double* __restrict__ scalars, unsigned long long* __restrict__ ticket) {
+  __shared__ double wsum[8];
+  __shared__ bool last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c = chunk_lo + blockIdx.x;
   const int64_t lo = c * kReduceChunk;
   int64_t hi = lo + kReduceChunk;
   if (hi > rest_hi) hi = rest_hi;
   const double* a = rest + (lo - rest_lo);
   const int64_t len = hi - lo;
-  double res;
   if (len == kReduceChunk) {
-    const double* p = a + lane * 128;
-    double r[8];
+    const int leaf = tid >> 3, j = tid & 7;
+    const double* pl = a + leaf * 128 + j;
+    double r = pl[0];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = p[j];
-#pragma unroll 4
-    for (int i = 8; i < 128; i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] += p[i + j];
+    for (int i = 8; i < 128; i += 8) r += pl[i];
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 4);
+    // leaves 4w .. 4w + 3 sit at lanes 0, 8, 16, 24 of warp w
+    r += __shfl_xor_sync(0xffffffffu, r, 8);
+    r += __shfl_xor_sync(0xffffffffu, r, 16);
+    if (lane == 0) wsum[warp] = r;
+    __syncthreads();
+    if (tid == 0) {
+      const double s01 = wsum[0] + wsum[1], s23 = wsum[2] + wsum[3];
+      const double s45 = wsum[4] + wsum[5], s67 = wsum[6] + wsum[7];
+      partials[c - chunk_lo] = (s01 + s23) + (s45 + s67);
     }
-    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) res += __shfl_xor_sync(0xffffffffu, res, off);
-  } else {
-    res = lane == 0 ? pairwise_rec(a, len) : 0.0;
+  } else if (tid == 0) {
+    partials[c - chunk_lo] = pairwise_rec(a, len);
   }
-  if (lane == 0) partials[c - chunk_lo] = res;
+  if (!ticket) return;
+  if (tid == 0) {
+    __threadfence();
+    const unsigned long long t = atomicAdd(ticket, 1ull);
+    last = t == (unsigned long long)(gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && tid == 0) {
+    __threadfence();
+    const volatile double* pv = partials;
+    double sum = 0.0;
+    for (int64_t k = 0; k < (int64_t)gridDim.x; ++k) sum += pv[k];
+    scalars[0] = scalars[1] + sum;
+    *ticket = 0ull;
+  }
 }
 
-// total = block_first + ((0 + p0) + p1) + ...   (vg/vecchia.py:213, :174-177)
-__global__ void total_kernel(const double* __restrict__ partials, int64_t nchunks,
-                             double* __restrict__ scalars) {
-  double s = 0.0;
-  for (int64_t c = 0; c < nchunks; ++c) s += partials[c];
-  scalars[0] = scalars[1] + s;
-}
+// total with no chunks (a plan of the joint block only): total = block_first
+__global__ void total_kernel(double* __restrict__ scalars) { scalars[0] = scalars[1] + 0.0; }
 
 __global__ void scatter_partials_kernel(const double* __restrict__ partials, int64_t nch,
                                         int64_t chunk_lo, int has_first,
@@ -123,13 +146,16 @@ cudaError_t launch_permute_obs(const double* d_obs, const int64_t* d_order, int6
 
 cudaError_t launch_reduce(const Plan& p, bool want_total, cudaStream_t stream) {
   int64_t nch = p.chunk_hi - p.chunk_lo;
+  // d_scalars[3]: the last-CTA ticket (zeroed at plan creation, rearmed by
+  // the last CTA)
+  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(p.d_scalars + 3);
   if (nch > 0) {
-    const int warps = 4;
-    unsigned blocks = (unsigned)((nch + warps - 1) / warps);
-    chunk_partials_kernel<<<blocks, warps * 32, 0, stream>>>(p.d_rest, p.rest_lo, p.rest_hi,
-                                                             p.chunk_lo, p.chunk_hi, p.d_partials);
+    chunk_partials_kernel<<<(unsigned)nch, 256, 0, stream>>>(p.d_rest, p.rest_lo, p.rest_hi, p.chunk_lo,
+                                                             p.chunk_hi, p.d_partials, p.d_scalars,
+                                                             want_total ? ticket : nullptr);
+  } else if (want_total) {
+    total_kernel<<<1, 1, 0, stream>>>(p.d_scalars);
   }
-  if (want_total) total_kernel<<<1, 1, 0, stream>>>(p.d_partials, nch, p.d_scalars);
   return cudaGetLastError();
 }
 
