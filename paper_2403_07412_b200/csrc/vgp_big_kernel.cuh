@@ -35,7 +35,10 @@
 
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "vgp_ktab.cuh"
 #include "vgp_math.cuh"
@@ -58,6 +61,7 @@ using ws::tidx;
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kGroup = 4;  // tiles per warp in flight
+constexpr int kTraceCtas = 16, kTraceEv = 6;
 constexpr int kHead = 256 + 64 + 8 + 5 * kBesselTab;  // exp table | Lt | Iv | Bessel tables
 
 __host__ __device__ constexpr int ntiles_of(int m) { return (m + 2 + 7) / 8; }
@@ -131,14 +135,15 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
   return cov_ref(cp, d);
 }
 
-template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false>
+template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false, bool TRACE = false>
 __global__ void __launch_bounds__(kThreads, GT ? 3 : (SLOTS && MC == 120 ? 5 : 4))
 loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __restrict__ nbr,
                   int m_rt, int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
                   double* __restrict__ sig_out, unsigned long long* __restrict__ fail,
                   const double* __restrict__ dcache, int64_t cstride, double* __restrict__ gscratch,
-                  const double* __restrict__ ktab, const __grid_constant__ SlotMap smap) {
+                  const double* __restrict__ ktab, const __grid_constant__ SlotMap smap,
+                  long long* __restrict__ trace = nullptr) {
   // MC > 0: conditioning size fixed at compile time (tile counts and
   // addresses fold to constants)
   const int m = MC > 0 ? MC : m_rt;
@@ -156,6 +161,13 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
   double* T = GT ? gscratch + (size_t)blockIdx.x * tile_doubles(m) : smem + head_doubles(m, KIND);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // clock64 phase trace (VGP_TRACE_BIG, tools/big_trace.py): CTAs <
+  // kTraceCtas, their third block, per column and warp kTraceEv events
+  int iter = 0;
+  auto stamp = [&](int c, int ev) {
+    if (TRACE && iter == 2 && blockIdx.x < kTraceCtas && lane == 0)
+      trace[((blockIdx.x * kWarps + warp) * 32 + c) * kTraceEv + ev] = clock64();
+  };
   const int r = lane >> 2;  // fragment row
   const int q = lane & 3;   // fragment column pair
 
@@ -296,6 +308,7 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
     __syncthreads();
     for (int c = 0; c < NC; ++c) {
       const bool lastc = (c == NC - 1);
+      stamp(c, 0);
       if (kLookAhead) {
         if (warp != 0 && !lastc) column_work(c + 1, c - 1, 1, kWarps - 1);
       } else if (c > 0) {
@@ -400,7 +413,9 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
           }
         }
       }
+      stamp(c, 1);
       __syncthreads();
+      stamp(c, 2);
       if (lastc) break;
 
       // ================= solve the rows below the diagonal tile =================
@@ -440,12 +455,16 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
           }
         }
       }
+      stamp(c, 3);
       __syncthreads();
+      stamp(c, 4);
       if (kLookAhead) {
         column_finish(c + 1, c);
+        stamp(c, 5);
         __syncthreads();
       }
     }
+    ++iter;
   }
 }
 
@@ -480,13 +499,13 @@ inline bool use_global_tiles(int m) {
 // (x, y, obs, 0), one row per box, for tile::gather4
 bool point_map(const double4* pts, int64_t n, CUtensorMap* map);
 
-template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false>
+template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false, bool TRACE = false>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
-                   cudaStream_t stream, double* gscratch, int max_grid) {
+                   cudaStream_t stream, double* gscratch, int max_grid, long long* trace = nullptr) {
   CUtensorMap map;
   if (!point_map(p.d_pts, p.n, &map)) return cudaErrorNotSupported;
   const size_t sm = smem_bytes(p.m, GT, KIND, SLOTS);
-  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC, SLOTS>;
+  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC, SLOTS, TRACE>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (err != cudaSuccess) return err;
   int per_sm = 0;
@@ -502,8 +521,32 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   kern<<<grid, kThreads, sm, stream>>>(map, p.d_nbr, p.m, e_lo, e_hi, p.rest_lo, cp,
                                        p.d_rest, p.d_mu, p.d_sig, p.d_fail,
                                        p.d_dcache, p.dcache_stride, gscratch,
-                                       (KIND == kMaternGen && !p.no_ktab) ? p.d_ktab : nullptr, smap);
+                                       (KIND == kMaternGen && !p.no_ktab) ? p.d_ktab : nullptr, smap,
+                                       trace);
   return cudaGetLastError();
+}
+
+// VGP_TRACE_BIG=<file>: run the launch with the clock64 phase trace and
+// append it (diagnostics; tools/big_trace.py)
+template <int KIND, bool CACHE, bool GT, int MC, bool SLOTS>
+cudaError_t launch_traced(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+                          cudaStream_t stream, double* gscratch, int max_grid, const char* path) {
+  const size_t n = (size_t)kTraceCtas * kWarps * 32 * kTraceEv;
+  long long* d = nullptr;
+  cudaError_t err = cudaMalloc(&d, n * sizeof(long long));
+  if (err != cudaSuccess) return err;
+  err = cudaMemsetAsync(d, 0, n * sizeof(long long), stream);
+  if (err == cudaSuccess) err = launch<KIND, CACHE, GT, MC, SLOTS, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid, d);
+  std::vector<long long> h(n);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(h.data(), d, n * sizeof(long long), cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+  cudaFree(d);
+  if (err != cudaSuccess) return err;
+  if (FILE* f = std::fopen(path, "a")) {
+    for (size_t i = 0; i < n; ++i) std::fprintf(f, "%lld%c", h[i], (i + 1) % kTraceEv ? ' ' : '\n');
+    std::fclose(f);
+  }
+  return cudaSuccess;
 }
 
 template <int KIND>
@@ -521,7 +564,11 @@ cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_
   }
   // config 4 (m = 120, closed forms, distances from coordinates): compile-time
   // m, slot layout (4 CTAs per SM instead of 3)
-  if (p.m == 120 && KIND <= kMatern25) return launch<KIND, false, false, 120, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  if (p.m == 120 && KIND <= kMatern25) {
+    if (const char* path = std::getenv("VGP_TRACE_BIG"))
+      return launch_traced<KIND, false, false, 120, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid, path);
+    return launch<KIND, false, false, 120, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  }
   if (gt) return launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
   return slots ? launch<KIND, false, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
                : launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);

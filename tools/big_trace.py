@@ -6,7 +6,8 @@
 Per column c and warp: t0 column start, t1 phase-1 work done (warp 0:
 diagonal tile; warps 1-3: look-ahead column c+1), t2 after the barrier,
 t3 solve done, t4 after the barrier, t5 finish done (next column's t0 is
-after the third barrier)."""
+after the third barrier).  Post-barrier stamps are unreliable (the barrier
+blocks at the next instruction), so phases are measured between arrivals."""
 import os
 import sys
 
@@ -41,21 +42,19 @@ def show(path):
     a = a[-CTAS * W * 32:].reshape(CTAS, W, 32, EV)[:, :, :NC]
     ok = [b for b in range(CTAS) if (a[b, :, :NC - 1] > 0).all()]
     a = a[ok]
-    t0 = a[:, 0, 0, 0]
-    total = (a[:, 0, NC - 1, 2] - t0)
-    print(f"{len(ok)} CTAs; block time mean {total.mean():.0f} cycles")
-    ph1_d = a[:, 0, :, 1] - a[:, 0, :, 0]
-    ph1_la = (a[:, 1:, :, 1] - a[:, 1:, :, 0]).max(1)
-    bar1 = a[:, :, :, 2].max(1) - a[:, :, :, 1].max(1)
-    solve = (a[:, :, :, 3] - a[:, :, :, 2]).max(1)
-    fin = (a[:, :, :, 5] - a[:, :, :, 4]).max(1)
-    col = np.diff(a[:, 0, :, 0], axis=1)
-    print("col  diag  LAmax  bar1  solve  finish  column")
-    for c in range(NC):
-        print(f"{c:3d} {ph1_d[:, c].mean():6.0f} {ph1_la[:, c].mean():6.0f} {bar1[:, c].mean():5.0f}"
-              f" {solve[:, c].mean():6.0f} {fin[:, c].mean():6.0f} {col[:, c].mean() if c < NC - 1 else 0:7.0f}")
-    print("sum  ", ph1_d[:, :].mean(0).sum().round(), ph1_la.mean(0).sum().round(), bar1.mean(0).sum().round(),
-          solve[:, :NC - 1].mean(0).sum().round(), fin[:, :NC - 1].mean(0).sum().round())
+    # (BAR.SYNC.DEFER_BLOCKING: a warp blocks at the instruction after the
+    # barrier, so post-barrier stamps are not used; phases end at the last
+    # warp's arrival)
+    arr1 = a[:, :, :, 1].max(1)
+    diag = (a[:, 0, :, 1] - a[:, 0, :, 0]).mean(0)
+    la = (a[:, 1:, :, 1] - a[:, 1:, :, 0]).max(1).mean(0)
+    solve = (a[:, :, :, 3].max(1) - arr1).mean(0)
+    fin = (a[:, :, :, 5].max(1) - a[:, :, :, 3].max(1)).mean(0)
+    col = np.diff(a[:, 0, :, 0], axis=1).mean(0)
+    print(f"{len(ok)} CTAs; block {(a[:, 0, NC - 1, 1] - a[:, 0, 0, 0]).mean():.0f} cycles")
+    print("col  diag(w0)  lookahead(w1-3 max)  solve  finish  column")
+    for c in range(NC - 1):
+        print(f"{c:3d} {diag[c]:8.0f} {la[c]:12.0f} {solve[c]:12.0f} {fin[c]:7.0f} {col[c]:7.0f}")
 
 
 if __name__ == "__main__":
