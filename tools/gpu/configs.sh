@@ -4,5 +4,5 @@ timeout 900 python tools/mle_runs.py c5 --out gpurun_out/r02_mle_c5_ktab.jsonl >
 for cfg in "--n 4000000 --m 120" "--n 2000000 --locations clustered --ordering maxmin --nu 0.8"; do
   timeout 900 python bench.py $cfg --steps 10 --warmup 3 --e2e-steps 3 >> gpurun_out/r02_bench_configs.jsonl 2>gpurun_out/bench_cfg.err; echo "cfg rc=$?"
 done
-bash tools/gpu_sweep.sh 10 20 30 45 60 90 120 150 200 300 400 > gpurun_out/sweep.txt 2>&1; cat gpurun_out/sweep.txt
+bash tools/gpu/sweep.sh 10 20 30 45 60 90 120 150 200 300 400 > gpurun_out/sweep.txt 2>&1; cat gpurun_out/sweep.txt
 cat gpurun_out/sweep_m*.log | grep '^{' > gpurun_out/r02_sweep_c3_n250k.jsonl

@@ -1,5 +1,5 @@
 # ncu --set full of the non-headline kernels (one launch each), summarised on the box
-# usage: bash tools/r02_prof_aux.sh "name regex mode" ...  e.g.
+# usage: bash tools/gpu/prof_aux.sh "name regex mode" ...  e.g.
 #   "r02_ncu_knn_grid grid_query knn" "r02_ncu_dcache build_dcache dcache"
 #   "r02_ncu_tiny_m10 loglik_tiny m10" "r02_ncu_dmma_m20 ^loglik_kernel m20"
 #   "r02_ncu_ws_m30 loglik_ws_kernel m30" "r02_ncu_maxmin maxmin_cluster maxmin"

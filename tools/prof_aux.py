@@ -1,5 +1,5 @@
 """One invocation of a non-headline kernel, for `ncu -k regex:<kernel> -c 1`
-(tools/r02_prof_aux.sh): the kNN grid query and the distance-cache build of
+(tools/gpu/prof_aux.sh): the kNN grid query and the distance-cache build of
 config 2, the maxmin ordering of config 5, the small-m likelihood kernels of
 the config-3 sweep.
 
