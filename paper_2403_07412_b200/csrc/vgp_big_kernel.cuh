@@ -215,72 +215,73 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
     const double y_t = G[m].z;  // target observation (G is refilled before the last panel)
     fj = -1;
 
-    // tile column J of the block: generate the tiles (I, J), I >= J, dealt
-    // round-robin over warps [w0, w0 + nw) in groups of kGroup (inactive
-    // slots issue nothing), apply L of tile columns k <= kmax with DMMA and
-    // stage them (natural column order)
-    auto column_work = [&](const int J, const int kmax, const int w0, const int nw) {
-        for (int I0 = J + (warp - w0); I0 < NT; I0 += nw * kGroup) {
-          // active tiles of this group (warp-uniform), dispatched to a body
-          // unrolled for exactly that many: a predicated-off DMMA still
-          // occupies the FP64 datapath (ncu: 2464 DMMA issued per m = 120
-          // block against 1360 needed when the tail groups were predicated)
-          const int ng = min(kGroup, (NT - 1 - I0) / nw + 1);
-          auto group = [&](auto ngc) {
-            constexpr int NG = decltype(ngc)::value;
-            double acc[NG][2];
+    // tiles (I0 + g * st, J), g < NG: generate, apply L of tile columns
+    // k <= kmax with DMMA, stage (natural column order)
+    auto la_tiles = [&](const int J, const int kmax, const int I0, const int st, auto ngc) {
+      constexpr int NG = decltype(ngc)::value;
+      double acc[NG][2];
 #pragma unroll
-            for (int g = 0; g < NG; ++g) {
-              const int I = I0 + g * nw;
-              const int i = 8 * I + r;
-              double v0, v1;
-              const int j0 = 8 * J + 2 * q;  // columns j0, j0 + 1
-              if (CACHE) {
-                const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, J, NT) * 64 + chunk_off(r, q)));
-                v0 = cov_any<KIND>(dv.x, cp, tab, Bt, ktab);
-                v1 = cov_any<KIND>(dv.y, cp, tab, Bt, ktab);
-              } else {
-                const double2 pa = *reinterpret_cast<const double2*>(G + (i < P ? i : 0));
-                const double2 pb0 = *reinterpret_cast<const double2*>(G + j0);
-                const double2 pb1 = *reinterpret_cast<const double2*>(G + j0 + 1);
-                double dx = pa.x - pb0.x, dy = pa.y - pb0.y;
-                v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt, ktab);
-                dx = pa.x - pb1.x;
-                dy = pa.y - pb1.y;
-                v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt, ktab);
-              }
-              if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
-                v0 = (i == m + 1 && j0 < m) ? G[j0].z : 0.0;
-                v1 = (i == m + 1 && j0 + 1 < m) ? G[j0 + 1].z : 0.0;
-              }
-              // accumulate -A + sum L L^T and negate once at the store:
-              // bit-identical to A - sum L L^T (round-to-nearest is odd under
-              // negation) without negating an operand per DMMA
-              acc[g][0] = -v0;
-              acc[g][1] = -v1;
-            }
-            for (int k = 0; k <= kmax; ++k) {
-              const double2 b = ld2(tile(J, k) + chunk_off(r, q));
-              double2 a[NG];
-#pragma unroll
-              for (int g = 0; g < NG; ++g) a[g] = ld2(tile(I0 + g * nw, k) + chunk_off(r, q));
-#pragma unroll
-              for (int kk = 0; kk < 2; ++kk) {
-#pragma unroll
-                for (int g = 0; g < NG; ++g) mma(acc[g][0], acc[g][1], kk ? a[g].y : a[g].x, kk ? b.y : b.x);
-              }
-            }
-#pragma unroll
-            for (int g = 0; g < NG; ++g) st2(tile(I0 + g * nw, J) + chunk_off(r, q), -acc[g][0], -acc[g][1]);
-          };
-          static_assert(kGroup == 4, "group dispatch below");
-          switch (ng) {
-            case 4: group(std::integral_constant<int, 4>{}); break;
-            case 3: group(std::integral_constant<int, 3>{}); break;
-            case 2: group(std::integral_constant<int, 2>{}); break;
-            default: group(std::integral_constant<int, 1>{}); break;
-          }
+      for (int g = 0; g < NG; ++g) {
+        const int I = I0 + g * st;
+        const int i = 8 * I + r;
+        double v0, v1;
+        const int j0 = 8 * J + 2 * q;  // columns j0, j0 + 1
+        if (CACHE) {
+          const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (size_t)tidx(I, J, NT) * 64 + chunk_off(r, q)));
+          v0 = cov_any<KIND>(dv.x, cp, tab, Bt, ktab);
+          v1 = cov_any<KIND>(dv.y, cp, tab, Bt, ktab);
+        } else {
+          const double2 pa = *reinterpret_cast<const double2*>(G + (i < P ? i : 0));
+          const double2 pb0 = *reinterpret_cast<const double2*>(G + j0);
+          const double2 pb1 = *reinterpret_cast<const double2*>(G + j0 + 1);
+          double dx = pa.x - pb0.x, dy = pa.y - pb0.y;
+          v0 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt, ktab);
+          dx = pa.x - pb1.x;
+          dy = pa.y - pb1.y;
+          v1 = cov_any<KIND>(sqrt_pos_nz(fma(dx, dx, fma(dy, dy, 0x1p-1000))), cp, tab, Bt, ktab);
         }
+        if (i > m) {  // row m+1: yJ (0 from column m on); padding: 0
+          v0 = (i == m + 1 && j0 < m) ? G[j0].z : 0.0;
+          v1 = (i == m + 1 && j0 + 1 < m) ? G[j0 + 1].z : 0.0;
+        }
+        // accumulate -A + sum L L^T and negate once at the store:
+        // bit-identical to A - sum L L^T (round-to-nearest is odd under
+        // negation) without negating an operand per DMMA
+        acc[g][0] = -v0;
+        acc[g][1] = -v1;
+      }
+      for (int k = 0; k <= kmax; ++k) {
+        const double2 b = ld2(tile(J, k) + chunk_off(r, q));
+        double2 a[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) a[g] = ld2(tile(I0 + g * st, k) + chunk_off(r, q));
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+          for (int g = 0; g < NG; ++g) mma(acc[g][0], acc[g][1], kk ? a[g].y : a[g].x, kk ? b.y : b.x);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < NG; ++g) st2(tile(I0 + g * st, J) + chunk_off(r, q), -acc[g][0], -acc[g][1]);
+    };
+    // a group of ng tiles runs a body unrolled for exactly that many: a
+    // predicated-off DMMA still occupies the FP64 datapath (ncu: 2464 DMMA
+    // issued per m = 120 block against 1360 needed when the tail groups were
+    // predicated)
+    auto dispatch = [&](const int ng, auto&& body) {
+      static_assert(kGroup == 4, "group dispatch below");
+      switch (ng) {
+        case 4: body(std::integral_constant<int, 4>{}); break;
+        case 3: body(std::integral_constant<int, 3>{}); break;
+        case 2: body(std::integral_constant<int, 2>{}); break;
+        default: body(std::integral_constant<int, 1>{}); break;
+      }
+    };
+    // tiles (I, J), J <= I < Iend, dealt round-robin over warps
+    // [w0, w0 + nw) in groups of kGroup
+    auto column_work = [&](const int J, const int kmax, const int w0, const int nw, const int Iend) {
+      for (int I0 = J + (warp - w0); I0 < Iend; I0 += nw * kGroup)
+        dispatch(min(kGroup, (Iend - 1 - I0) / nw + 1), [&](auto ngc) { la_tiles(J, kmax, I0, nw, ngc); });
     };
     // the last left-looking step of tile column J: reload, apply L of column
     // k, stage (tiles dealt round-robin over all warps)
@@ -304,15 +305,19 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
     // (global-memory tiles, m >~ 230: no look-ahead, the extra reload pass
     // costs more in L2 than the overlap gains)
     constexpr bool kLookAhead = !GT;
-    column_work(0, -1, 0, kWarps);
+    auto la_rest = [&](const int c) { return min(max(NT - c - 1 - 3 * kGroup, 0), 3); };
+    column_work(0, -1, 0, kWarps, NT);
     __syncthreads();
     for (int c = 0; c < NC; ++c) {
       const bool lastc = (c == NC - 1);
       stamp(c, 0);
       if (kLookAhead) {
-        if (warp != 0 && !lastc) column_work(c + 1, c - 1, 1, kWarps - 1);
+        // (more than 12 tiles: warps 1..3 take 4 each and the diagonal warp,
+        // whose pivot chain is shorter than a 4-tile group's look-ahead
+        // (tools/big_trace.py), the last 1-3 after its panel)
+        if (warp != 0 && !lastc) column_work(c + 1, c - 1, 1, kWarps - 1, NT - la_rest(c));
       } else if (c > 0) {
-        column_work(c, c - 1, 0, kWarps);
+        column_work(c, c - 1, 0, kWarps, NT);
         __syncthreads();
       }
       // the last tile column is generated: G is free, gather the next block
@@ -412,6 +417,11 @@ loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __res
             }
           }
         }
+      }
+      if (kLookAhead && warp == 0 && !lastc) {
+        const int nr = la_rest(c);
+        if (nr > 0)
+          dispatch(nr, [&](auto ngc) { la_tiles(c + 1, c - 1, NT - nr, 1, ngc); });
       }
       stamp(c, 1);
       __syncthreads();
