@@ -632,8 +632,9 @@ def test_sphere_grid_knn_bit_exact(vg, monkeypatch, case, m):
 @pytest.mark.parametrize("name", golden_names("knn_sphere_big"))
 @pytest.mark.parametrize("grid", [True, False])
 def test_sphere_knn_at_scale_vs_reference(vg, monkeypatch, name, grid):
-    """Great-circle neighbour tables at 30-40k points (global; a dense 2-degree
-    patch with many near-ties) against the reference's own tables (glibc sin
+    """Great-circle neighbour tables at 30-100k points (global; dense 2- and
+    4-degree patches with many near-ties, 100k points ~1.4 km apart) against
+    the reference's own tables (glibc sin
     keys, vg/geo.py:266-292), by sha256 of the whole table: the device key
     (CUDA sin) decides the same top-m sets."""
     import hashlib
