@@ -22,10 +22,10 @@ __global__ void ktab_build_kernel(CovParams cp, double* __restrict__ out) {
   for (int j = 0; j < N; ++j) {
     const double x = cos(kPi * (j + 0.5) / N);
     const double u = mid + hw * x;
-    // u >= 1: C(u) e^u / s2 (the evaluation multiplies by s2 e^-u);
+    // u >= 1: C(u) / s2 (the evaluation multiplies by s2);
     // u < 1: s2 - C(u), so the small deviation from s2 that a smooth kernel's
     // near-singular blocks hinge on is interpolated to RELATIVE accuracy
-    const double v = ex >= 0 ? cp.coef * pow(u, cp.nu) * bessel_k<true>(cp, u)
+    const double v = ex >= 0 ? cp.coef * pow(u, cp.nu) * bessel_k(cp, u)
                              : cp.s2 - cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k(cp, u);
     f[j] = v;
   }

@@ -7,10 +7,15 @@
 // segment a degree-7 polynomial in t in [-1, 1) interpolating at the
 // Chebyshev nodes (measured relative interpolation error <= 2e-15 against
 // scipy.special.kv, 7e-14 next to u = 2 where AMOS itself switches methods).
-// For u >= 1 the table holds C(u) e^u / s2 and the evaluation multiplies by
-// the lean s2 e^-u, so the polynomial only carries the algebraic factor; for
-// u < 1 it holds s2 - C(u), interpolated to relative accuracy (smooth kernels'
-// near-singular blocks hinge on that small deviation).
+// For u < 1 the table holds s2 - C(u), interpolated to relative accuracy
+// (smooth kernels' near-singular blocks hinge on that small deviation); for
+// u >= 1 it holds C(u) / s2 itself.  There the segment's relative width
+// 1/64 makes e^-u vary by at most e^(-u/64) across it, so the degree-7
+// interpolant's relative error is ~(u/128)^8 / (2^7 8!), largest in absolute
+// terms near u = 9 at ~2e-19 s2 — far below an ulp of the diagonal — and no
+// exp is evaluated per entry (round 2 first stored C e^u / s2 and multiplied
+// by a lean exp: ~10 more FP64 operations on ~9% of c5's entries, paid by
+// whole warps through divergence).
 //
 // Evaluation is integer bit work (segment = binade and top 6 mantissa bits;
 // t = u scaled into [128, 256) by exponent replacement minus an odd integer,
@@ -97,7 +102,7 @@ __device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ 
   p = fma(p, t, c23.x);
   p = fma(p, t, c01.y);
   p = fma(p, t, c01.x);
-  if (__builtin_expect(bex >= 1023, 0)) return p * e_neg(u);  // u >= 1: exp-scaled form
+  if (__builtin_expect(bex >= 1023, 0)) return p * cp.s2;  // u >= 1: C / s2
   return cp.s2 - p;
 }
 
