@@ -128,8 +128,7 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
   if (KIND == kMaternGen) {
     // per-evaluation polynomial table (vgp_ktab.cuh) when the plan built one
     if (ktab)
-      return cov_ktab(d * cp.inv_beta, ktab, cp,
-                      [&](double u) { return cov_lean<kMatern05>(u, 1.0, tab); });
+      return cov_ktab(d * cp.inv_beta, ktab, cp);
     return matern_gen(d, cp, btab);
   }
   return cov_ref(cp, d);

@@ -47,7 +47,7 @@ static __device__ __noinline__ double matern_gen_exact(double u, const CovParams
   return cp.s2 * cp.coef * pow(u, cp.nu) * bessel_k(cp, u);
 }
 
-// C(u) from the table; e_neg(u) must return s2 * e^-u (the caller's lean exp)
+// C(u) from the table
 // A kernel may stage a window of kKtabWinSeg consecutive segments (14
 // binades) in shared memory, starting at segment wseg0 (ktab_window); the
 // evaluation reads those with LDS, the rest from the global table.
@@ -63,10 +63,9 @@ inline int ktab_window(double dmax, double inv_beta) {
   return (lo - kKtabOMin) * kKtabSeg;
 }
 
-template <typename ExpNeg>
 __device__ __forceinline__ double cov_ktab(double u, const double* __restrict__ ktab,
-                                           const CovParams& cp, ExpNeg e_neg,
-                                           const double* ktw = nullptr, int wseg0 = 0) {
+                                           const CovParams& cp, const double* ktw = nullptr,
+                                           int wseg0 = 0) {
   const int hi = __double2hiint(u);
   const int lo = __double2loint(u);
   const int bex = hi >> 20;  // biased exponent (u >= 0)

@@ -66,14 +66,13 @@ constexpr int kTraceBlocks = ws::kTraceBlocks;
 constexpr int kTraceEvents = ws::kTraceEvents;
 
 // covariance at distance d: lean closed forms, or the general-nu Matern from
-// the per-evaluation polynomial table (vgp_ktab.cuh) with the same lean exp
+// the per-evaluation polynomial table (vgp_ktab.cuh)
 template <int KIND>
 __device__ __forceinline__ double cov_gen(double d, double inv_beta, const double* tab,
                                           const double* __restrict__ ktab, const CovParams& cp,
                                           const double* ktw = nullptr, int wseg0 = 0) {
   if constexpr (KIND != kMaternGen) return cov_lean<KIND>(d, inv_beta, tab);
-  return cov_ktab(d * inv_beta, ktab, cp,
-                  [&](double u) { return cov_lean<kMatern05>(u, 1.0, tab); }, ktw, wseg0);
+  return cov_ktab(d * inv_beta, ktab, cp, ktw, wseg0);
 }
 // the K_nu table window in shared memory (general nu, NT = 8: the smem left
 // beside the eight slots holds 14 binades)
