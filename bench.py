@@ -62,7 +62,9 @@ def fp64_peak():
                   "148 SMs @1965 MHz (profiles/r01_fp64_peak.jsonl)")
 
 
-KERNELS_PER_EVAL = 4  # joint block, fused block kernel, chunk partials, ordered total
+# joint block, fused block kernel, chunk partials (+ the ordered total in its
+# last CTA); general nu adds the per-evaluation K_nu table build
+KERNELS_PER_EVAL = 3
 
 
 def parse():
@@ -435,7 +437,7 @@ def run_ours_single(args):
         "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "paper_2403_07412_b200.vecchia_loglik(dataset, plan, spec)"},
-        "gpu_launches": KERNELS_PER_EVAL * args.steps,
+        "gpu_launches": (KERNELS_PER_EVAL + (args.nu not in (0.5, 1.5, 2.5))) * args.steps,
         "clocks": clk.summary(),
         "plan_s": round(knn_s, 3), "simulate_s": round(sim_s, 3), "total": total,
         "kernel_variant": VARIANT_NAMES.get(dp.kernel_variant, str(dp.kernel_variant)),
@@ -546,7 +548,7 @@ def run_ours_multi(args, rank, world):
             "e2e": {"value": 1.0 / e2e_s, "unit": "evals/s",
                     "h2d_bytes_per_step": args.n * 24, "d2h_bytes_per_step": 8 * (sh.buf.numel()),
                     "api": "paper_2403_07412_b200.distributed.ShardedVecchia"},
-            "gpu_launches": (KERNELS_PER_EVAL + 1) * args.steps,
+            "gpu_launches": (KERNELS_PER_EVAL + 1 + (args.nu not in (0.5, 1.5, 2.5))) * args.steps,
             "clocks": clk.summary(), "plan_s": round(knn_s, 3),
             "shard_plan_s": round(shard_plan_s, 3), "total": total,
             "collective": "1 NCCL all_reduce(SUM) of 1+n_chunks fp64 per eval",
