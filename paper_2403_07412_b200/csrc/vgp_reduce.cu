@@ -81,11 +81,23 @@ chunk_partials_kernel(const double* __restrict__ rest, int64_t rest_lo, int64_t 
     last = t == (unsigned long long)(gridDim.x - 1);
   }
   __syncthreads();
-  if (last && tid == 0) {
-    __threadfence();
-    const volatile double* pv = partials;
-    double sum = 0.0;
-    for (int64_t k = 0; k < (int64_t)gridDim.x; ++k) sum += pv[k];
+  if (!last) return;
+  // the last CTA: stage the partials in shared memory with all threads (one
+  // round trip instead of one per chunk), then add them in chunk order
+  __shared__ double buf[2048];
+  __threadfence();
+  const volatile double* pv = partials;
+  double sum = 0.0;
+  const int64_t nch = gridDim.x;
+  for (int64_t b0 = 0; b0 < nch; b0 += 2048) {
+    const int cnt = nch - b0 < 2048 ? (int)(nch - b0) : 2048;
+    __syncthreads();
+    for (int k = tid; k < cnt; k += blockDim.x) buf[k] = pv[b0 + k];
+    __syncthreads();
+    if (tid == 0)
+      for (int k = 0; k < cnt; ++k) sum += buf[k];
+  }
+  if (tid == 0) {
     scalars[0] = scalars[1] + sum;
     *ticket = 0ull;
   }
