@@ -44,6 +44,9 @@ def _read_csv(path: str, metric) -> geo.Dataset:
     return geo.Dataset(rows[:, :2], rows[:, 2], metric)
 
 
+_FUSED_INNER = 8
+
+
 def cmd_bench(args) -> dict:
     if not (1 <= args.m < args.n):
         raise ValueError(f"need 1 <= m < n, got m={args.m}, n={args.n}")
@@ -69,9 +72,13 @@ def cmd_bench(args) -> dict:
         t2 = time.perf_counter()
         res = vecchia._reduction_stage(ws, ordered.observations, plan.m, lower, mu_p, sig_p)
         t3 = time.perf_counter()
-        dp.launch(spec)  # the fused evaluation vecchia_loglik runs, device-resident
+        # the fused evaluation vecchia_loglik runs, device-resident; a few
+        # back-to-back launches per fetch so the host sync/launch latency does
+        # not mask the linear growth in n at small sizes
+        for _ in range(_FUSED_INNER):
+            dp.launch(spec)
         total = dp.fetch()[0]
-        t4 = time.perf_counter()
+        t4 = t3 + (time.perf_counter() - t3) / _FUSED_INNER
         if rep:
             for k, v in zip(phases, (t1 - t0, t2 - t1, t3 - t2)):
                 phases[k].append(v)

@@ -29,6 +29,14 @@
 // one block's chain factors panel c the worker prepares the other block's
 // column.  8 blocks in flight per SM (8 x 20.8 KB of shared memory).
 //
+// C0 (default for the cached closed forms at NT = 8): the chain generates its
+// block's tile column 0 itself, straight into its row-owner registers, right
+// after the previous block's epilogue; the worker starts every block at
+// column 1.  A clock64 trace showed the chains idle ~2.8k cycles per block
+// waiting for column 0 while the worker (never idle) finished the other
+// slot's last column and generated 8 tiles: 115.5 -> 123.1 evals/s (c2),
+// bit-identical.
+//
 // Shared memory per block: the tile triangle (tile (I, J) at
 // (J NT - J (J-1)/2 + I - J) * 64 doubles, column-major, ws::chunk_off swizzle: conflict-free fragment
 // and row accesses), staging S for the last panel (the tile triangle is then
@@ -91,7 +99,7 @@ __host__ __device__ constexpr SlotLayout slot_layout(int nt) {
 // the cached distances, one column ahead, in the time they otherwise wait for
 // their worker); the workers generate the other half and load these.
 __host__ __device__ constexpr bool chain_tile(int I, int c) { return ((I - c) & 1) == 0; }
-template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false>
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false, bool C0 = false>
 __global__ void __launch_bounds__(kThreads, 1)
 loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
                   int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
@@ -167,11 +175,11 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
       pf1[h] = pf0[h];
       const int64_t e = e0 + sl[h];
       if (e < e_hi) {
-        if (!CG && CACHE && lane == 0)
+        if (!CG && !C0 && CACHE && lane == 0)
           bulk_load(Tb(sl[h]), dcache + (e - 1 - rest_lo) * cstride, cbytes, MBb(sl[h]));
         pf0[h] = slot_point(slot_index(e, lane));
         if (P > 32) pf1[h] = slot_point(slot_index(e, lane + 32));
-        if (CG) {
+        if (CG || C0) {
           // the chain generates from O: stage it, then the distances (the
           // mbarrier's release by lane 0 after __syncwarp covers both)
           double* O = Ob(sl[h]);
@@ -196,7 +204,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
         mark(s, 1, 0);
         double* O = Ob(s);
         double2* XY = XYb(s);
-        if (!CG) {
+        if (!CG && !C0) {
           if (lane < P) O[lane] = lane < m ? pf0[h].z : 0.0;
           if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1[h].z : 0.0;
         }
@@ -222,7 +230,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
       __syncwarp();
 
 #pragma unroll
-      for (int c = 0; c < NT; ++c) {
+      for (int c = C0 ? 1 : 0; c < NT; ++c) {
         if (c < NC) {
           const bool lastc = (c == NC - 1);
 #pragma unroll
@@ -311,7 +319,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
               // T is no longer read for this block (the last panel runs from
               // S): stream in the next block's distances (CG: and its
               // observations, which the chain generates from)
-              if (CG && en < e_hi) {
+              if ((CG || C0) && en < e_hi) {
                 double* O = Ob(s);
                 if (lane < P) O[lane] = lane < m ? pf0[h].z : 0.0;
                 if (P > 32 && lane + 32 < P) O[lane + 32] = lane + 32 < m ? pf1[h].z : 0.0;
@@ -323,7 +331,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             // ---- hand column c over (natural column order); before a block's
             // first column, wait until the chain has taken the previous
             // block's last column (one arrival in flight per barrier; S reuse)
-            if (c == 0 && !first) bar_sync(2 * s + 1, 64);
+            if (!C0 && c == 0 && !first) bar_sync(2 * s + 1, 64);
 #pragma unroll
             for (int I = 0; I < NT; ++I) {
               if (I >= c) {
@@ -368,9 +376,11 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
     };
     for (int64_t e = e0 + s; e < e_hi; e += stride, par ^= 1, ++tblk) {
       int fj = -1;  // first non-positive pivot column
-      if (CG) {
+      if (CG || C0) {
         mbar_wait(MBb(s), dph);  // this block's distances and observations
         dph ^= 1;
+      }
+      if (CG) {
         gen_col(0);
         if (NC > 1) gen_col(1);
       }
@@ -382,7 +392,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
           const int NR = P - R0;
           const int jmax = min(8, m - R0);  // pivots in this tile column
           mark(s, 0, 2 * c);
-          bar_sync(2 * s, 64);
+          if (!(C0 && c == 0)) bar_sync(2 * s, 64);
           // lane owns panel rows R0 + lane + 32 rr: tile c + (lane + 32 rr) / 8, row lane & 7
           constexpr int kMaxRows = 2;
           double a[kMaxRows][8];
@@ -390,6 +400,31 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             const int I = c + ((lane + 32 * rr) >> 3);
             return lastc ? S + (I - c) * 64 : T + tidx(I < NT ? I : NT - 1, c, NT) * 64;
           };
+          if (C0 && c == 0) {
+            // C0: the chain generates tile column 0 itself, straight into its
+            // row-owner registers from the cached distances (the worker starts
+            // each block at column 1; column 0's distances are never read again
+            // and the tiles take L(., 0) as usual)
+#pragma unroll
+            for (int rr = 0; rr < kMaxRows; ++rr) {
+              const int row = lane + 32 * rr;
+              const int I = row >> 3;
+              const double* tp = T + tidx(I, 0, NT) * 64;
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const double2 dv = ld2(tp + chunk_off(lane & 7, x));
+                double v0 = cov_gen<KIND>(dv.x, inv_beta, tab, ktab, cpx, ktw, wseg0);
+                double v1 = cov_gen<KIND>(dv.y, inv_beta, tab, ktab, cpx, ktw, wseg0);
+                if (I == NT - 1 && row > m) {  // row m+1: yJ; padding: 0
+                  const double2 ov = ld2(Ob(s) + 2 * x);
+                  v0 = row == m + 1 ? ov.x : 0.0;
+                  v1 = row == m + 1 ? ov.y : 0.0;
+                }
+                a[rr][2 * x] = v0;
+                a[rr][2 * x + 1] = v1;
+              }
+            }
+          } else {
 #pragma unroll
           for (int rr = 0; rr < kMaxRows; ++rr) {
             if (rr * 32 < NR) {
@@ -404,9 +439,10 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
               }
             }
           }
+          }
           mark(s, 0, 2 * c + 1);
           // last column: rows are in registers, S may be refilled
-          if (lastc && e + stride < e_hi) bar_arrive(2 * s + 1, 64);
+          if (!C0 && lastc && e + stride < e_hi) bar_arrive(2 * s + 1, 64);
           double lastpiv = 1.0;
           if (jmax > 0) {
             double piv = shfl(a[0][0], 0);
@@ -504,7 +540,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   }
 }
 
-template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false>
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false, bool C0 = false>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, long long* trace = nullptr) {
   constexpr SlotLayout L = slot_layout(NT);
@@ -513,7 +549,7 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
                                       (kTabWindow<KIND, NT> ? (size_t)kKtabWinSeg * 8 : 0));
   static size_t configured[64] = {};
   const int dev = p.device & 63;
-  auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE, CG>;
+  auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE, CG, C0>;
   if (configured[dev] < sm) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
@@ -537,7 +573,8 @@ inline cudaError_t launch_traced(const Plan& p, const CovParams& cp, int64_t e_l
   cudaError_t err = cudaMalloc(&d, n * sizeof(long long));
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(d, 0, n * sizeof(long long), stream);
-  err = launch<8, kMatern15, 60, true, true>(p, cp, e_lo, e_hi, stream, d);
+  err = p.tune == 1 ? launch<8, kMatern15, 60, true, true>(p, cp, e_lo, e_hi, stream, d)
+                    : launch<8, kMatern15, 60, true, true, false, true>(p, cp, e_lo, e_hi, stream, d);
   std::vector<long long> h(n);
   if (err == cudaSuccess) err = cudaMemcpyAsync(h.data(), d, n * sizeof(long long), cudaMemcpyDeviceToHost, stream);
   if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
@@ -561,6 +598,11 @@ cudaError_t launch_c(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e
   // the closed forms it only lengthens the chains (c2: 115.8 -> 106.2)
   if (cache && (KIND == kMaternGen || p.tune == 2))
     return launch<NT, KIND, MC, true, false, true>(p, cp, e_lo, e_hi, stream);
+  // closed forms, NT = 8 (m = 55..62, so at least two tile columns): the chain
+  // generates tile column 0 itself (C0; VGP_TUNE=1 selects the previous layout)
+  if constexpr (NT == 8 && KIND != kMaternGen) {
+    if (cache && p.tune != 1) return launch<NT, KIND, MC, true, false, false, true>(p, cp, e_lo, e_hi, stream);
+  }
   if (cache) return launch<NT, KIND, MC, true>(p, cp, e_lo, e_hi, stream);
   return launch<NT, KIND, MC, false>(p, cp, e_lo, e_hi, stream);
 }
