@@ -779,3 +779,37 @@ def test_shard_plans_bitwise_on_one_gpu(vg, oracle, world):
             vec[0] = bf
         dp.close()
     assert ordered_total(vec) == full.total
+
+
+@pytest.mark.parametrize("m,nu", [(55, 0.5), (58, 1.5), (60, 2.5), (60, 1.5), (62, 0.5)])
+def test_chain_column0_layout_bitwise(vg, oracle, monkeypatch, m, nu):
+    """The m + 2 <= 64 kernel's default layout, where the chain generates tile
+    column 0 itself (C0), returns the same bits as the previous layout
+    (VGP_TUNE=1: the worker generates every column), including the per-block
+    arrays, and matches the oracle; several slots' blocks per CTA (n >> 8 x 148)."""
+    rng = np.random.default_rng(m)
+    n = 4000
+    locs = rng.random((n, 2))
+    spec = vg.KernelSpec("matern", vg.KernelParams(1.3, 0.07, nu))
+    # model-consistent observations (SURVEY.md H5): the oracle gate is 1e-9
+    plan = vg.make_plan(vg.Dataset(locs, np.zeros(n)), m, "random", seed=3)
+    y_ord = oracle.simulate_vecchia(locs[plan.permutation.order], m, plan.neighbors.neighbors,
+                                    "matern", 1.3, 0.07, nu, m + 7)
+    y = np.empty(n)
+    y[plan.permutation.order] = y_ord
+    data = vg.Dataset(locs, y)
+    res = {}
+    for tune in ("0", "1"):
+        monkeypatch.setenv("VGP_TUNE", tune)
+        plan = vg.make_plan(data, m, "random", seed=3)
+        dp = plan.device_plan()
+        dp.set_variant(8)
+        res[tune] = vg.vecchia_loglik(data, plan, spec)
+        assert dp.info()[8] == 1  # the distance cache is streamed (the C0 path)
+    monkeypatch.delenv("VGP_TUNE")
+    assert res["0"].total == res["1"].total
+    np.testing.assert_array_equal(res["0"].block_rest, res["1"].block_rest)
+    ordered = data.permute(plan.permutation)
+    ref = oracle.loglik(ordered.locations, ordered.observations, m, plan.neighbors.neighbors,
+                        "matern", 1.3, 0.07, nu)
+    assert rel(res["0"].total, ref.total) <= TOL_TOTAL
