@@ -98,8 +98,13 @@ __host__ __device__ constexpr SlotLayout slot_layout(int nt) {
 // CG: the chain warps generate half of the covariance tiles (in place over
 // the cached distances, one column ahead, in the time they otherwise wait for
 // their worker); the workers generate the other half and load these.
-__host__ __device__ constexpr bool chain_tile(int I, int c) { return ((I - c) & 1) == 0; }
-template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false, bool C0 = false>
+// CGK = 2: every other tile of a column; CGK = k > 2: all but every k-th tile
+template <int CGK = 2>
+__host__ __device__ constexpr bool chain_tile(int I, int c) {
+  return CGK == 2 ? ((I - c) & 1) == 0 : (I - c) % CGK != CGK - 1;
+}
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false, bool C0 = false,
+          int CGK = 2>
 __global__ void __launch_bounds__(kThreads, 1)
 loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ nbr, int m_rt,
                   int64_t e_lo, int64_t e_hi, int64_t rest_lo, double s2, double inv_beta,
@@ -256,7 +261,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
               ++gcnt[h];
 #pragma unroll
               for (int I = 0; I < NT; ++I) {
-                if (I >= c && chain_tile(I, c)) {
+                if (I >= c && chain_tile<CGK>(I, c)) {
                   const double2 v = ld2(T + tidx(I, c, NT) * 64 + chunk_off(r, q));
                   acc[I][0] = v.x;
                   acc[I][1] = v.y;
@@ -265,7 +270,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
             }
 #pragma unroll
             for (int I = 0; I < NT; ++I) {
-              if (I >= c && !(CG && chain_tile(I, c))) {
+              if (I >= c && !(CG && chain_tile<CGK>(I, c))) {
                 const int i = 8 * I + r;
                 double v0, v1;
                 if (CACHE) {
@@ -356,7 +361,7 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
     auto gen_col = [&](const int c) {
 #pragma unroll
       for (int I = 0; I < NT; ++I) {
-        if (I >= c && chain_tile(I, c)) {
+        if (I >= c && chain_tile<CGK>(I, c)) {
           const int i = 8 * I + r;
           double* tp = T + tidx(I, c, NT) * 64 + chunk_off(r, q);
           const double2 dv = ld2(tp);
@@ -540,7 +545,8 @@ loglik_ws3_kernel(const double4* __restrict__ pts, const int32_t* __restrict__ n
   }
 }
 
-template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false, bool C0 = false>
+template <int NT, int KIND, int MC, bool CACHE, bool TRACE = false, bool CG = false, bool C0 = false,
+          int CGK = 2>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, long long* trace = nullptr) {
   constexpr SlotLayout L = slot_layout(NT);
@@ -549,7 +555,7 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
                                       (kTabWindow<KIND, NT> ? (size_t)kKtabWinSeg * 8 : 0));
   static size_t configured[64] = {};
   const int dev = p.device & 63;
-  auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE, CG, C0>;
+  auto kern = loglik_ws3_kernel<NT, KIND, MC, CACHE, TRACE, CG, C0, CGK>;
   if (configured[dev] < sm) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
@@ -566,15 +572,19 @@ cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_h
   return cudaGetLastError();
 }
 
-inline cudaError_t launch_traced(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
+template <int KIND>
+cudaError_t launch_traced(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                                  cudaStream_t stream, const char* path) {
   const size_t n = (size_t)kSlots * 2 * kTraceBlocks * kTraceEvents;
   long long* d = nullptr;
   cudaError_t err = cudaMalloc(&d, n * sizeof(long long));
   if (err != cudaSuccess) return err;
   cudaMemsetAsync(d, 0, n * sizeof(long long), stream);
-  err = p.tune == 1 ? launch<8, kMatern15, 60, true, true>(p, cp, e_lo, e_hi, stream, d)
-                    : launch<8, kMatern15, 60, true, true, false, true>(p, cp, e_lo, e_hi, stream, d);
+  if constexpr (KIND == kMaternGen)
+    err = launch<8, KIND, 60, true, true, true, false, 3>(p, cp, e_lo, e_hi, stream, d);
+  else
+    err = p.tune == 1 ? launch<8, KIND, 60, true, true>(p, cp, e_lo, e_hi, stream, d)
+                      : launch<8, KIND, 60, true, true, false, true>(p, cp, e_lo, e_hi, stream, d);
   std::vector<long long> h(n);
   if (err == cudaSuccess) err = cudaMemcpyAsync(h.data(), d, n * sizeof(long long), cudaMemcpyDeviceToHost, stream);
   if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
@@ -590,12 +600,20 @@ inline cudaError_t launch_traced(const Plan& p, const CovParams& cp, int64_t e_l
 template <int NT, int KIND, int MC>
 cudaError_t launch_c(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                      cudaStream_t stream, bool cache) {
-  if (NT == 8 && KIND == kMatern15 && MC == 60 && cache) {
-    if (const char* path = std::getenv("VGP_TRACE3")) return launch_traced(p, cp, e_lo, e_hi, stream, path);
+  if constexpr (NT == 8 && (KIND == kMatern15 || KIND == kMaternGen) && MC == 60) {
+    if (cache) {
+      if (const char* path = std::getenv("VGP_TRACE3")) return launch_traced<KIND>(p, cp, e_lo, e_hi, stream, path);
+    }
   }
   // general nu: covariance generation (the K_nu table) is the expensive part,
   // so the chains generate in their idle time (c5: 12.2 -> 15.4 evals/s); for
   // the closed forms it only lengthens the chains (c2: 115.8 -> 106.2)
+  // (the chains take 2 of every 3 tiles: they wait ~2.4k cycles per column
+  // while the worker never does -- c5 18.64 -> 18.9 evals/s against every
+  // other tile; 3 of 4: 18.65)
+  if constexpr (KIND == kMaternGen) {
+    if (cache && p.tune != 7) return launch<NT, KIND, MC, true, false, true, false, 3>(p, cp, e_lo, e_hi, stream);
+  }
   if (cache && (KIND == kMaternGen || p.tune == 2))
     return launch<NT, KIND, MC, true, false, true>(p, cp, e_lo, e_hi, stream);
   // closed forms, NT = 8 (m = 55..62, so at least two tile columns): the chain
