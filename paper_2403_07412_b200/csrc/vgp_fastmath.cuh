@@ -4,6 +4,7 @@
 // special-case branches, and spends at most a third of libdevice's FP64
 // instructions:
 //   sqrt_pos      MUFU.RSQ64H seed + two Newton steps on the root    6 FP64
+//   sqrt_pos_nz   MUFU.RSQ64H seed + one third-order step             5 FP64
 //   rsqrt_pos     MUFU.RSQ64H seed + two Newton steps                 8 FP64
 //   exp_neg_tab   exp(-u) = T[j] * p(r) * 2^e, 256-entry 2^(j/256)
 //                 table, Cody-Waite reduction, degree-4 polynomial     9 FP64
@@ -33,14 +34,15 @@ __device__ __forceinline__ double sqrt_pos(double x) {
 
 // sqrt(x) for normal x > 0 (no zero guard: callers add 2^-1000 to squared
 // distances, so exact duplicates come out as d ~ 1e-150, i.e. C(d) = C(0)).
+// One third-order step on s = x y0: sqrt(x) = s (1 - e)^(-1/2) with
+// e = 1 - s y0 (the rounding of s cancels), truncated after 3 e^2 / 8
+// (|e| < 2^-21, so the next term is ~2^-65): 5 FP64, 4 deep.
 __device__ __forceinline__ double sqrt_pos_nz(double x) {
   const double y = rsqrt_seed(x);
-  const double h = 0.5 * y;
-  double s = x * y;
-  double r = fma(-s, s, x);
-  s = fma(r, h, s);
-  r = fma(-s, s, x);
-  return fma(r, h, s);
+  const double s = x * y;
+  const double e = fma(-s, y, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  return fma(s * e, p, s);
 }
 
 // 1/sqrt(x) for normal x > 0.
