@@ -134,8 +134,10 @@ __device__ __forceinline__ double cov_any(double d, const CovParams& cp, const d
   return cov_ref(cp, d);
 }
 
-template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false, bool TRACE = false>
-__global__ void __launch_bounds__(kThreads, GT ? 3 : (SLOTS && MC == 120 ? 5 : 4))
+// MINB > 0: minimum resident CTAs for the register budget (5 where the tile
+// triangle lets 5 CTAs share the SM, e.g. m = 63..80)
+template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false, bool TRACE = false, int MINB = 0>
+__global__ void __launch_bounds__(kThreads, MINB > 0 ? MINB : (GT ? 3 : (SLOTS && MC == 120 ? 5 : 4)))
 loglik_big_kernel(const __grid_constant__ CUtensorMap pmap, const int32_t* __restrict__ nbr,
                   int m_rt, int64_t e_lo, int64_t e_hi, int64_t rest_lo, CovParams cp,
                   double* __restrict__ rest, double* __restrict__ mu_out,
@@ -508,13 +510,13 @@ inline bool use_global_tiles(int m) {
 // (x, y, obs, 0), one row per box, for tile::gather4
 bool point_map(const double4* pts, int64_t n, CUtensorMap* map);
 
-template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false, bool TRACE = false>
+template <int KIND, bool CACHE, bool GT, int MC = 0, bool SLOTS = false, bool TRACE = false, int MINB = 0>
 cudaError_t launch(const Plan& p, const CovParams& cp, int64_t e_lo, int64_t e_hi,
                    cudaStream_t stream, double* gscratch, int max_grid, long long* trace = nullptr) {
   CUtensorMap map;
   if (!point_map(p.d_pts, p.n, &map)) return cudaErrorNotSupported;
   const size_t sm = smem_bytes(p.m, GT, KIND, SLOTS);
-  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC, SLOTS, TRACE>;
+  auto kern = loglik_big_kernel<KIND, CACHE, GT, MC, SLOTS, TRACE, MINB>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (err != cudaSuccess) return err;
   int per_sm = 0;
@@ -579,8 +581,15 @@ cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_
     return launch<KIND, false, false, 120, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
   }
   if (gt) return launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
-  return slots ? launch<KIND, false, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid)
-               : launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  if (slots) return launch<KIND, false, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  // closed forms whose triangle lets 5 CTAs share the SM: a 5-CTA register
+  // budget (96 registers; n = 250k: m = 64 156 -> 170, m = 75 132 -> 144
+  // evals/s; at m = 90, 4 CTAs by shared memory, it only spills)
+  if constexpr (KIND <= kMatern25) {
+    if (ctas_per_sm(smem_bytes(p.m, false, KIND), 8) >= 5 && p.tune != 11)
+      return launch<KIND, false, false, 0, false, false, 5>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  }
+  return launch<KIND, false, false>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
 }
 
 }  // namespace big
