@@ -498,7 +498,9 @@ inline int ctas_per_sm(size_t bytes, int cap = 4) {  // by shared memory (228 KB
 }
 // the slot layout only where it buys resident CTAs (its lookups cost ~6%)
 inline bool use_slots(int m, int kind) {
-  return ctas_per_sm(smem_bytes(m, false, kind, true)) > ctas_per_sm(smem_bytes(m, false, kind, false));
+  // (up to 5 resident CTAs for the closed forms, whose 96-register budget allows 5)
+  const int cap = kind <= kMatern25 ? 5 : 4;
+  return ctas_per_sm(smem_bytes(m, false, kind, true), cap) > ctas_per_sm(smem_bytes(m, false, kind, false), cap);
 }
 // tiles in shared memory up to ~200 KB per CTA (compacted when that fits),
 // else the global scratch
@@ -581,7 +583,13 @@ cudaError_t launch_kind(const Plan& p, const CovParams& cp, int64_t e_lo, int64_
     return launch<KIND, false, false, 120, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
   }
   if (gt) return launch<KIND, false, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
-  if (slots) return launch<KIND, false, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  if (slots) {
+    if constexpr (KIND <= kMatern25) {
+      if (ctas_per_sm(smem_bytes(p.m, false, KIND, true), 8) >= 5 && p.tune != 11)
+        return launch<KIND, false, false, 0, true, false, 5>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+    }
+    return launch<KIND, false, false, 0, true>(p, cp, e_lo, e_hi, stream, gscratch, max_grid);
+  }
   // closed forms whose triangle lets 5 CTAs share the SM: a 5-CTA register
   // budget (96 registers; n = 250k: m = 64 156 -> 170, m = 75 132 -> 144
   // evals/s; at m = 90, 4 CTAs by shared memory, it only spills)
